@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""bench.py — device-timed KV-cache scoring → routing → count pass (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ko|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (one rank per GPU, NCCL)
+
+A step = one pass of the whole hot path over one batch of synthetic input resident in HBM:
+ko_score_batch over every tuple (all ops × all variants in one read of each tuple's KV, margins,
+every plan of the config's grid evaluated per tuple, integer counts) plus, at N > 1, the NCCL
+all-reduce of the int64 count vector.  Weak scaling: each rank owns a distinct shard of
+n_tuples tuples (tuple ids rank·n .. rank·n + n − 1), so value = N·n_tuples·K / max-rank time.
+
+`--impl reference` times the reference arm of this tier: the fp64 CPU oracle (oracle/) as it
+stands, on this host's cores, on a bounded sample of the same workload per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tuples scored/sec and % of HBM peak at 1/2/4/8 B200 vs CPU oracle"
+UNIT = "tuples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--n-tuples", type=int, default=0, help="override tuples per rank")
+    ap.add_argument("--impl", default="ko", choices=["ko", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="CPU work budget of the oracle sample (cpu_baseline / reference arm)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------
+# helpers
+# ------------------------------------------------------------------------------------------
+def n_kept(L, keep):
+    return np.maximum(1, (L.astype(np.int64) * keep) // 1000)
+
+
+def algorithmic_bytes(wl, seq_len, n_plans):
+    """Σ_t Σ_l Hkv·4·d·need(t,l) (need = largest prefix any variant with cut > l
+    consults; nested prefixes count once) + 4 B per page-table entry + 4 B seq_len + 8 B indptr
+    + 1 B per gold byte + 4 B per margin and class written."""
+    sp = wl.spec
+    need_tokens = 0
+    for l in range(sp.n_layers):
+        ks = [k for (k, c) in wl.variants if c > l]
+        if ks:
+            need_tokens += int(n_kept(seq_len, max(ks)).sum())
+    kv = need_tokens * sp.n_kv_heads * 4 * sp.head_dim
+    n = len(seq_len)
+    pages = int(((seq_len.astype(np.int64) + 15) // 16).sum())
+    meta = 4 * pages + 12 * n
+    gold = sp.n_ops * n
+    out = 8 * sp.n_ops * len(wl.variants) * n
+    return kv + meta + gold + out, kv
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload_key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(workload_key)
+    return None if e is None else e.get("dram_bytes_per_launch")
+
+
+def oracle_sample(wl, seconds, rank_offset=0):
+    """Time the oracle as it stands on a bounded, deterministic sample of the workload."""
+    import oracle
+    import kogen
+    threads = len(os.sched_getaffinity(0))
+    ops = oracle.workload_ops(wl)
+    done, t_used, batch, start_t = 0, 0.0, 16, rank_offset
+    stride = max(1, wl.n_tuples // 997)
+    while t_used < seconds and done < wl.n_tuples:
+        tids = (start_t + (np.arange(done, done + batch) * stride)) % (wl.n_tuples * 1000)
+        pool, indptr, ids, sl = kogen.host_pool(wl.spec, tids)
+        t0 = time.perf_counter()
+        m, c = oracle.score(wl.spec, pool, indptr, ids, sl, ops, wl.variants, n_threads=threads)
+        gold = np.zeros((wl.spec.n_ops, len(tids)), np.uint8)
+        oracle.run_plans(wl.plans, m, c, wl.spec.op_classes, gold)
+        t_used += time.perf_counter() - t0
+        done += batch
+        batch = min(256, batch * 2)
+    return dict(value=done / t_used, unit=UNIT, cores=threads, kind="oracle",
+                sample=f"{done} tuples of {wl.name} (every {stride}-th id), all ops x variants "
+                       f"scored + {len(wl.plans)} plans, fp64, input generation excluded",
+                seconds=round(t_used, 2))
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm: the oracle on the host cores
+# ------------------------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from kogen import workloads
+    wl = workloads.get(args.config)
+    per_step = args.cpu_seconds / max(1, args.steps + args.warmup)
+    per_step = max(per_step, 0.5)
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = oracle_sample(wl, per_step, rank_offset=i * 7919)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = float(np.mean(vals))
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.desc}", "mode": wl.mode,
+                       "sample": "bounded per-step sample, host cores"},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# product arm
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_2602_04430_b200 as ko
+    from kogen import workloads
+    from kogen.device import device_workload
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl = workloads.get(args.config)
+    n = args.n_tuples or wl.n_tuples
+    t0 = rank * n
+    d = device_workload(wl, t0=t0, n=n, placement="contiguous")
+    kv, ops, gold = d["kv"], d["ops"], d["gold"]
+    n_var, n_ops = len(wl.variants), wl.spec.n_ops
+    plans = wl.plans
+    margins = torch.empty((n_ops, n_var, n), dtype=torch.float32, device="cuda")
+    classes = torch.empty((n_ops, n_var, n), dtype=torch.int32, device="cuda")
+    counts = torch.zeros((len(plans), ko.COUNTS_PER_PLAN), dtype=torch.int64, device="cuda")
+    ws = ko.alloc_workspace(kv, ops, n_var, n)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        counts.zero_()
+        ko.score_batch(kv, ops, wl.variants, margins=margins, classes=classes, plans=plans,
+                       gold=gold, counts=counts, workspace=ws)
+        if dist is not None:
+            dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+
+    # kernel-only events: the library records them around its hot kernel (ko_set_trace_events)
+    ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(args.steps)]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for i in range(args.steps):
+            ko.set_trace_events(ev_pairs[i][0], ev_pairs[i][1])
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ko.set_trace_events(None, None)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_pairs]))
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * n * args.steps / (ms_total / 1000.0)
+
+    # parity spot-check of the timed outputs: counts == oracle plan evaluation of the GPU margins
+    cnt = counts.cpu().numpy()
+    alg_bytes, kv_bytes = algorithmic_bytes(wl, d["seq_len"], len(plans))
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
+    key = f"{wl.name}:{n}"
+    traffic = ncu_traffic(key)
+
+    # e2e: the same pass through the public API from pinned host buffers, H2D inside the region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, ko, torch, wl, d, ops, gold, plans, margins, classes, counts, ws, world,
+                      dist)
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = oracle_sample(wl, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.desc}", "n_tuples_per_rank": n,
+                       "mode": "grid (all ops x variants in one read + per-tuple plan grid)",
+                       "n_plans": len(plans), "variants": wl.variants,
+                       "kv_bytes_per_rank": kv_bytes,
+                       "l2": "inputs larger than L2 (KV per rank >> 126 MB); no flush",
+                       "parallelism": f"dp{world} (tuple shards, NCCL all-reduce of counts)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "ko_score_kernel", "kernel_ms": kern_ms,
+                         "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+            "cpu_baseline": cb,
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.summary(),
+            "counts_plan0": cnt[0, :5].tolist(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, ko, torch, wl, d, ops, gold, plans, margins, classes, counts, ws, world, dist):
+    """E2E: host (pinned) KV pages → device in tuple chunks on a copy stream, overlapped with
+    scoring of the previous chunk on the compute stream; D2H of counts and margins each step."""
+    kv = d["kv"]
+    n = kv.n_tuples
+    try:
+        host_pool = torch.empty(kv.pool.shape, dtype=kv.pool.dtype, pin_memory=True)
+    except RuntimeError as e:  # noqa: BLE001
+        return {"value": None, "unit": UNIT, "error": f"pinned host alloc failed: {e}"[:200]}
+    host_pool.copy_(kv.pool)               # fill the host copy (outside the timed region)
+    h_margins = torch.empty(margins.shape, dtype=margins.dtype, pin_memory=True)
+    h_counts = torch.empty(counts.shape, dtype=counts.dtype, pin_memory=True)
+    indptr = d["indptr"]
+    n_chunks = 8
+    bounds = np.linspace(0, n, n_chunks + 1).astype(np.int64)
+    chunk_idx = [torch.arange(int(a), int(b), dtype=torch.int32, device="cuda")
+                 for a, b in zip(bounds[:-1], bounds[1:])]
+    copy_s = torch.cuda.Stream()
+    comp_s = torch.cuda.current_stream()
+    page_bytes = kv.pool[0].numel() * kv.pool.element_size()
+
+    def e2e_step():
+        counts.zero_()
+        evs = []
+        for c in range(n_chunks):
+            p0, p1 = int(indptr[bounds[c]]), int(indptr[bounds[c + 1]])
+            with torch.cuda.stream(copy_s):
+                kv.pool[p0:p1].copy_(host_pool[p0:p1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_s)
+            evs.append(ev)
+        for c in range(n_chunks):
+            comp_s.wait_event(evs[c])
+            ko.score_batch(kv, ops, wl.variants, tuple_idx=chunk_idx[c], margins=margins,
+                           classes=classes, plans=plans, gold=gold, counts=counts, workspace=ws)
+        if dist is not None:
+            dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+        h_counts.copy_(counts, non_blocking=True)
+        h_margins.copy_(margins, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp_s)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record(comp_s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    h2d = int(indptr[-1]) * page_bytes
+    d2h = h_counts.numel() * 8 + h_margins.numel() * 4
+    del host_pool
+    return {"value": world * n * args.e2e_steps / (ms / 1000.0), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+            "ms_per_step": ms / args.e2e_steps,
+            "how": "pinned host KV pages -> device in 8 tuple chunks on a copy stream, "
+                   "overlapped with ko_score_batch on each landed chunk; counts+margins D2H"}
+
+
+if __name__ == "__main__":
+    main()

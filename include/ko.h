@@ -178,14 +178,22 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
                           int32_t n_variants, int64_t n_tuples, const uint8_t* gold,
                           int64_t* counts, void* stream);
 
-/* Bytes of workspace ko_score_batch needs for this shape (n_work = number of tuples processed). */
-size_t ko_workspace_size(const ko_kv_cache* kv, int32_t n_ops, int32_t n_variants, int64_t n_work);
+/* Bytes of device workspace ko_score_batch needs for this shape (n_work = number of tuples it
+ * will process: n_idx, or n_tuples when tuple_idx is NULL).  Returns 0 on invalid arguments. */
+size_t ko_workspace_size(const ko_kv_cache* kv, const ko_operator* ops, int32_t n_ops,
+                         int32_t n_variants, int64_t n_work);
 
 /* Host helper (not GPU work): Bayesian lower bound of Eqs. recall-lower-bound /
  * precision-lower-bound: the (1 − alpha) quantile of Beta(1 + a, 1 + b), i.e.
  * ℓ_α = I^{-1}(1 − α; 1 + a, 1 + b) (Q7).  recall: (a, b) = (TP, FN); precision: (TP, FP).
  * Returns NaN on invalid input (a < 0, b < 0, alpha outside (0,1)).                           */
 double ko_beta_lower_bound(int64_t a, int64_t b, double alpha);
+
+/* Tracing hook (runtime profiling): when ev_begin/ev_end (cudaEvent_t handles) are non-NULL,
+ * every later ko_score_batch call on this thread records ev_begin on its stream immediately before
+ * its first scoring-kernel launch and ev_end immediately after its last one, so a caller can time
+ * the hot kernel alone with cudaEventElapsedTime.  Pass NULL, NULL to disable. */
+void ko_set_trace_events(void* ev_begin, void* ev_end);
 
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char* ko_last_error(void);

@@ -1,0 +1,279 @@
+"""paper_2602_04430_b200 — thin Python binding of libko.so (include/ko.h).
+
+Argument marshalling only: every step of the scoring → routing → count pass runs in the sm_100a
+kernels of ``csrc/``.  torch supplies device memory and streams; there is no CPU fallback — if
+``lib/libko.so`` is missing, importing this package raises.
+
+Names mirror the C ABI: ``score_batch`` ↔ ``ko_score_batch``, ``route`` ↔ ``ko_route``,
+``reduce_stats`` ↔ ``ko_reduce_stats``, ``workspace_size``, ``beta_lower_bound``, ``last_error``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libko.so")
+
+PAGE_TOKENS = 16
+MAX_OPS, MAX_VARIANTS, MAX_STAGES, MAX_PLANS, MAX_CLASSES, MAX_ROWS = 4, 8, 8, 64, 8, 16
+COUNTS_PER_PLAN = 5 + 4 * MAX_STAGES
+C_TP, C_FP, C_FN, C_OUT, C_GOLD = 0, 1, 2, 3, 4
+STATUS = {0: "KO_OK", 1: "KO_EINVAL", 2: "KO_EUNSUPPORTED", 3: "KO_ECUDA", 4: "KO_EWORKSPACE"}
+
+
+class KoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _KV(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+                ("gqa_group", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("n_q", ctypes.c_int32), ("kv_pool", ctypes.c_void_p), ("n_pages", ctypes.c_int64),
+                ("page_indptr", ctypes.c_void_p), ("page_ids", ctypes.c_void_p),
+                ("seq_len", ctypes.c_void_p), ("n_tuples", ctypes.c_int64)]
+
+
+class _Op(ctypes.Structure):
+    _fields_ = [("n_classes", ctypes.c_int32), ("q", ctypes.c_void_p), ("w", ctypes.c_void_p),
+                ("b", ctypes.c_void_p)]
+
+
+class _Variant(ctypes.Structure):
+    _fields_ = [("keep_permille", ctypes.c_int32), ("layer_cut", ctypes.c_int32)]
+
+
+class _Stage(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("variant", ctypes.c_int32),
+                ("theta_lo", ctypes.c_float), ("theta_hi", ctypes.c_float),
+                ("is_final", ctypes.c_int32)]
+
+
+class _Plan(ctypes.Structure):
+    _fields_ = [("n_stages", ctypes.c_int32), ("stage", _Stage * MAX_STAGES)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    L.ko_score_batch.argtypes = [ctypes.POINTER(_KV), P, I32, P, I32, P, I64, P, P, P, I32, P, P,
+                                 P, ctypes.c_size_t, P]
+    L.ko_score_batch.restype = ctypes.c_int
+    L.ko_route.argtypes = [P, P, P, P, I32, I32, I64, I32, P, P, P, P, P, P]
+    L.ko_route.restype = ctypes.c_int
+    L.ko_reduce_stats.argtypes = [P, I32, P, P, P, I32, I32, I64, P, P, P]
+    L.ko_reduce_stats.restype = ctypes.c_int
+    L.ko_workspace_size.argtypes = [ctypes.POINTER(_KV), P, I32, I32, I64]
+    L.ko_workspace_size.restype = ctypes.c_size_t
+    L.ko_beta_lower_bound.argtypes = [I64, I64, ctypes.c_double]
+    L.ko_beta_lower_bound.restype = ctypes.c_double
+    L.ko_set_trace_events.argtypes = [P, P]
+    L.ko_set_trace_events.restype = None
+    L.ko_last_error.restype = ctypes.c_char_p
+    L.ko_version.restype = ctypes.c_char_p
+    return L
+
+
+_lib = _load()
+EXPORTS = ("ko_score_batch", "ko_route", "ko_reduce_stats", "ko_workspace_size",
+           "ko_beta_lower_bound", "ko_set_trace_events", "ko_last_error", "ko_version")
+
+
+def lib():
+    return _lib
+
+
+def last_error() -> str:
+    return _lib.ko_last_error().decode()
+
+
+def version() -> str:
+    return _lib.ko_version().decode()
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise KoError(rc, last_error())
+
+
+# ---------------------------------------------------------------------------------------------
+# descriptors
+# ---------------------------------------------------------------------------------------------
+@dataclass
+class KVCache:
+    """Device tensors of one importance-ordered paged KV store (ko_kv_cache)."""
+    pool: "torch.Tensor"          # bf16/uint16/int16 [n_pages][n_layers][2][n_kv_heads][16][D]
+    page_indptr: "torch.Tensor"   # int64 [n_tuples+1]
+    page_ids: "torch.Tensor"      # int32 [nnz]
+    seq_len: "torch.Tensor"       # int32 [n_tuples]
+    n_layers: int
+    n_kv_heads: int
+    gqa_group: int
+    head_dim: int
+    n_q: int = 1
+
+    @property
+    def n_tuples(self) -> int:
+        return int(self.seq_len.numel())
+
+    def _c(self) -> _KV:
+        for name in ("pool", "page_indptr", "page_ids", "seq_len"):
+            t = getattr(self, name)
+            if not t.is_cuda:
+                raise ValueError(f"KVCache.{name} must be a CUDA tensor (no CPU path)")
+        return _KV(self.n_layers, self.n_kv_heads, self.gqa_group, self.head_dim, self.n_q,
+                   self.pool.data_ptr(), int(self.pool.shape[0]), self.page_indptr.data_ptr(),
+                   self.page_ids.data_ptr(), self.seq_len.data_ptr(), self.n_tuples)
+
+
+@dataclass
+class Operator:
+    """One logical operator (ko_operator): n_classes 1 = filter, >= 2 = map-classify."""
+    n_classes: int
+    q: "torch.Tensor"   # bf16 [n_layers][Hq][n_q][D]
+    w: "torch.Tensor"   # fp32 [n_classes][n_layers][Hq][n_q][D]
+    b: "torch.Tensor"   # fp32 [n_classes]
+
+
+Stage = Tuple[int, int, float, float, int]
+
+
+def _ops(ops: Sequence[Operator]):
+    arr = (_Op * len(ops))()
+    for i, o in enumerate(ops):
+        for name in ("q", "w", "b"):
+            if not getattr(o, name).is_cuda:
+                raise ValueError(f"Operator.{name} must be a CUDA tensor")
+        arr[i] = _Op(int(o.n_classes), o.q.data_ptr(), o.w.data_ptr(), o.b.data_ptr())
+    return arr
+
+
+def _variants(vs: Sequence[Tuple[int, int]]):
+    return (_Variant * len(vs))(*[_Variant(int(k), int(c)) for k, c in vs])
+
+
+def make_plans(plans: Sequence[Sequence[Stage]]):
+    arr = (_Plan * max(1, len(plans)))()
+    for g, pl in enumerate(plans):
+        if not 1 <= len(pl) <= MAX_STAGES:
+            raise ValueError(f"plan {g}: {len(pl)} stages")
+        arr[g].n_stages = len(pl)
+        for s, (op, var, lo, hi, fin) in enumerate(pl):
+            arr[g].stage[s] = _Stage(int(op), int(var), float(lo), float(hi), int(fin))
+    return arr
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# ---------------------------------------------------------------------------------------------
+# entry points
+# ---------------------------------------------------------------------------------------------
+def workspace_size(kv: KVCache, ops: Sequence[Operator], n_variants: int, n_work: int) -> int:
+    return int(_lib.ko_workspace_size(ctypes.byref(kv._c()), _ops(ops), len(ops), n_variants,
+                                      n_work))
+
+
+def alloc_workspace(kv: KVCache, ops: Sequence[Operator], n_variants: int, n_work: int):
+    import torch
+    n = workspace_size(kv, ops, n_variants, n_work)
+    if n == 0:
+        raise KoError(1, last_error() or "invalid arguments to ko_workspace_size")
+    # torch's caching allocator returns ≥ 512-byte aligned blocks
+    return torch.empty(n, dtype=torch.uint8, device=kv.pool.device)
+
+
+def score_batch(kv: KVCache, ops: Sequence[Operator], variants: Sequence[Tuple[int, int]],
+                tuple_idx=None, margins=None, classes=None, plans=None, gold=None, counts=None,
+                workspace=None, stream=None, want_classes: bool = True):
+    """ko_score_batch.  Returns (margins, classes, counts) device tensors (allocated here when not
+    given; counts are accumulated into a given tensor)."""
+    import torch
+    dev = kv.pool.device
+    n_ops, n_var, n = len(ops), len(variants), kv.n_tuples
+    routed = plans is not None and len(plans) == 1
+    if margins is None:
+        margins = torch.empty((n_ops, n_var, n), dtype=torch.float32, device=dev)
+    if classes is None and want_classes:
+        classes = torch.empty((n_ops, n_var, n), dtype=torch.int32, device=dev)
+    n_plans = 0 if plans is None else len(plans)
+    if counts is None and n_plans:
+        counts = torch.zeros((n_plans, COUNTS_PER_PLAN), dtype=torch.int64, device=dev)
+    n_work = n if tuple_idx is None else int(tuple_idx.numel())
+    if workspace is None:
+        workspace = alloc_workspace(kv, ops, n_var, n_work)
+    parr = make_plans(plans) if n_plans else None
+    rc = _lib.ko_score_batch(ctypes.byref(kv._c()), _ops(ops), n_ops, _variants(variants), n_var,
+                             _ptr(tuple_idx), n_work if tuple_idx is not None else 0,
+                             _ptr(margins), _ptr(classes), parr, n_plans, _ptr(gold),
+                             _ptr(counts), workspace.data_ptr(), workspace.numel(),
+                             _stream(stream))
+    _check(rc)
+    return margins, classes, counts
+
+
+def route(plan: Sequence[Stage], margins, classes, n_classes: Sequence[int], stage: int,
+          tuple_state, worklist=None, worklist_len=None, gold=None, counts=None, stream=None):
+    """ko_route.  tuple_state (uint32 as int32 tensor) is updated in place."""
+    import torch
+    n_ops, n_var, n = margins.shape
+    if counts is None:
+        counts = torch.zeros((1, COUNTS_PER_PLAN), dtype=torch.int64, device=margins.device)
+    nc = (ctypes.c_int32 * n_ops)(*[int(c) for c in n_classes])
+    rc = _lib.ko_route(make_plans([plan]), margins.data_ptr(), _ptr(classes), nc, n_ops, n_var, n,
+                       stage, tuple_state.data_ptr(), _ptr(worklist), _ptr(worklist_len),
+                       _ptr(gold), counts.data_ptr(), _stream(stream))
+    _check(rc)
+    return counts
+
+
+def reduce_stats(plans: Sequence[Sequence[Stage]], margins, classes, n_classes: Sequence[int],
+                 gold=None, counts=None, stream=None):
+    """ko_reduce_stats: per-plan count rows on precomputed margins."""
+    import torch
+    n_ops, n_var, n = margins.shape
+    if counts is None:
+        counts = torch.zeros((len(plans), COUNTS_PER_PLAN), dtype=torch.int64,
+                             device=margins.device)
+    nc = (ctypes.c_int32 * n_ops)(*[int(c) for c in n_classes])
+    rc = _lib.ko_reduce_stats(make_plans(plans), len(plans), margins.data_ptr(), _ptr(classes),
+                              nc, n_ops, n_var, n, _ptr(gold), counts.data_ptr(), _stream(stream))
+    _check(rc)
+    return counts
+
+
+def set_trace_events(ev_begin=None, ev_end=None) -> None:
+    """ko_set_trace_events: torch.cuda.Event pair recorded around the hot kernel of later
+    score_batch calls on this thread (None, None disables)."""
+    import torch
+    def handle(ev):
+        if ev is None:
+            return None
+        if ev.cuda_event == 0:          # torch creates the CUDA event lazily on first record
+            ev.record(torch.cuda.current_stream())
+        return ev.cuda_event
+    _lib.ko_set_trace_events(handle(ev_begin), handle(ev_end))
+
+
+def beta_lower_bound(a: int, b: int, alpha: float) -> float:
+    """ℓ_α = I^{-1}(1 − α; 1 + a, 1 + b) (Eqs. recall/precision lower bound)."""
+    return float(_lib.ko_beta_lower_bound(int(a), int(b), float(alpha)))
+
+
+def abi_ok() -> bool:
+    """True when every symbol include/ko.h declares is exported by the loaded library."""
+    return all(hasattr(_lib, s) for s in EXPORTS)

@@ -1,0 +1,491 @@
+// ko_api.cpp — the C ABI of libko.so (include/ko.h): host validation, workspace layout, and the
+// orchestration of the sm_100a kernels in ko_kernels.cu.  No allocation happens in a call; every
+// launch goes on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "ko.h"
+#include "ko_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local cudaEvent_t g_trace_begin = nullptr, g_trace_end = nullptr;
+
+ko_status fail(ko_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+ko_status fail(ko_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define KO_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e__ = (expr);                                                          \
+    if (e__ != cudaSuccess) return fail(KO_ECUDA, "%s: %s", #expr, cudaGetErrorString(e__)); \
+  } while (0)
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int pow2_at_least(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+ko_status validate_kv(const ko_kv_cache* kv) {
+  if (!kv) return fail(KO_EINVAL, "kv is NULL");
+  if (!kv->kv_pool || !kv->page_indptr || !kv->page_ids || !kv->seq_len)
+    return fail(KO_EINVAL, "kv: NULL pool/page_indptr/page_ids/seq_len");
+  if (kv->head_dim != 64 && kv->head_dim != 128)
+    return fail(KO_EINVAL, "head_dim %d not in {64,128}", kv->head_dim);
+  if (kv->n_layers < 1 || kv->n_kv_heads < 1 || kv->gqa_group < 1 || kv->n_q < 1)
+    return fail(KO_EINVAL, "kv: n_layers/n_kv_heads/gqa_group/n_q must be >= 1");
+  if (kv->n_tuples < 0 || kv->n_pages < 0) return fail(KO_EINVAL, "kv: negative sizes");
+  if (kv->n_tuples > 0x7fffffffll) return fail(KO_EUNSUPPORTED, "n_tuples > 2^31-1");
+  if (((uintptr_t)kv->kv_pool & 15) != 0) return fail(KO_EINVAL, "kv_pool not 16-byte aligned");
+  return KO_OK;
+}
+
+ko_status validate_ops(const ko_kv_cache* kv, const ko_operator* ops, int32_t n_ops) {
+  if (!ops || n_ops < 1 || n_ops > KO_MAX_OPS)
+    return fail(KO_EINVAL, "n_ops %d outside [1,%d]", n_ops, KO_MAX_OPS);
+  for (int o = 0; o < n_ops; ++o) {
+    if (!ops[o].q || !ops[o].w || !ops[o].b) return fail(KO_EINVAL, "op %d: NULL q/w/b", o);
+    if (ops[o].n_classes < 1) return fail(KO_EINVAL, "op %d: n_classes < 1", o);
+    if (ops[o].n_classes > KO_MAX_CLASSES)
+      return fail(KO_EUNSUPPORTED, "op %d: n_classes %d > %d", o, ops[o].n_classes, KO_MAX_CLASSES);
+  }
+  if ((int64_t)kv->gqa_group * kv->n_q > KO_MAX_ROWS)
+    return fail(KO_EUNSUPPORTED, "gqa_group*n_q = %d > %d", kv->gqa_group * kv->n_q, KO_MAX_ROWS);
+  return KO_OK;
+}
+
+ko_status validate_variants(const ko_kv_cache* kv, const ko_variant* v, int32_t n) {
+  if (!v || n < 1 || n > KO_MAX_VARIANTS)
+    return fail(KO_EINVAL, "n_variants %d outside [1,%d]", n, KO_MAX_VARIANTS);
+  for (int i = 0; i < n; ++i) {
+    if (v[i].keep_permille < 1 || v[i].keep_permille > 1000)
+      return fail(KO_EINVAL, "variant %d: keep_permille %d outside [1,1000]", i, v[i].keep_permille);
+    if (v[i].layer_cut < 1 || v[i].layer_cut > kv->n_layers)
+      return fail(KO_EINVAL, "variant %d: layer_cut %d outside [1,%d]", i, v[i].layer_cut,
+                  kv->n_layers);
+  }
+  return KO_OK;
+}
+
+ko_status validate_plan(const ko_plan* P, int g, const int32_t* n_classes, int32_t n_ops,
+                        int32_t n_variants) {
+  if (P->n_stages < 1 || P->n_stages > KO_MAX_STAGES)
+    return fail(KO_EINVAL, "plan %d: n_stages %d outside [1,%d]", g, P->n_stages, KO_MAX_STAGES);
+  int final_at[KO_MAX_OPS];
+  for (int o = 0; o < KO_MAX_OPS; ++o) final_at[o] = -2;  // -2: unreferenced, -1: no final yet
+  for (int s = 0; s < P->n_stages; ++s) {
+    const ko_stage& st = P->stage[s];
+    if (st.op < 0 || st.op >= n_ops) return fail(KO_EINVAL, "plan %d stage %d: op %d", g, s, st.op);
+    if (st.variant < 0 || st.variant >= n_variants)
+      return fail(KO_EINVAL, "plan %d stage %d: variant %d", g, s, st.variant);
+    if (!(st.theta_lo <= st.theta_hi))
+      return fail(KO_EINVAL, "plan %d stage %d: theta_lo > theta_hi (or NaN)", g, s);
+    if (final_at[st.op] >= 0)
+      return fail(KO_EINVAL, "plan %d stage %d: op %d has a stage after its final stage", g, s,
+                  st.op);
+    if (final_at[st.op] == -2) final_at[st.op] = -1;
+    if (st.is_final) {
+      if (n_classes[st.op] <= 1 && st.theta_lo != st.theta_hi)
+        return fail(KO_EINVAL, "plan %d stage %d: final filter stage needs theta_lo == theta_hi",
+                    g, s);
+      final_at[st.op] = s;
+    }
+  }
+  for (int o = 0; o < n_ops; ++o)
+    if (final_at[o] == -1) return fail(KO_EINVAL, "plan %d: op %d has no final stage", g, o);
+  return KO_OK;
+}
+
+struct Workspace {
+  unsigned long long* unit_counter;
+  unsigned long long* worklist_len;
+  int32_t* done;
+  float* part;
+  uint4* qfrag;
+  uint4* wfrag;
+  uint32_t* tuple_state;
+  int32_t* worklist;
+  size_t total;
+};
+
+// Layout: [counters 256 B][done][part][qfrag][wfrag][tuple_state][worklist]
+Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_variants,
+                 int64_t n_work, uint8_t* base) {
+  Workspace w{};
+  const int CPR = pow2_at_least(max_cls);
+  const int KS = kv->head_dim / 16;
+  const int NT = 2 * CPR;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return base ? base + o : nullptr;
+  };
+  uint8_t* ctr = take(256);
+  w.unit_counter = (unsigned long long*)ctr;
+  w.worklist_len = ctr ? (unsigned long long*)(ctr + 8) : nullptr;
+  w.done = (int32_t*)take(sizeof(int32_t) * (size_t)std::max<int64_t>(n_work, 1));
+  w.part = (float*)take(sizeof(float) * (size_t)std::max<int64_t>(n_work, 1) * kv->n_layers *
+                        kv->n_kv_heads * n_ops * n_variants * CPR);
+  w.qfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * KS * 32);
+  w.wfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * NT * KS * 32);
+  w.tuple_state = (uint32_t*)take(sizeof(uint32_t) * (size_t)std::max<int64_t>(kv->n_tuples, 1));
+  w.worklist = (int32_t*)take(sizeof(int32_t) * (size_t)std::max<int64_t>(kv->n_tuples, 1));
+  w.total = off;
+  return w;
+}
+
+int max_classes(const ko_operator* ops, int n_ops) {
+  int m = 1;
+  for (int o = 0; o < n_ops; ++o) m = std::max(m, (int)ops[o].n_classes);
+  return m;
+}
+
+// fill the kv/op/variant part of ScoreParams and the matching PrepParams for a set of local ops
+void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
+                 const ko_operator* ops, const int* op_sel, int n_sel, const ko_variant* variants,
+                 const int* var_sel, int n_vsel, int32_t n_ops_total, int32_t n_var_total,
+                 const Workspace& ws, int CPR, int NH) {
+  std::memset(&sp, 0, sizeof(sp));
+  std::memset(&pp, 0, sizeof(pp));
+  sp.pool = (const uint16_t*)kv->kv_pool;
+  sp.page_elems = (int64_t)kv->n_layers * 2 * kv->n_kv_heads * KO_PAGE_TOKENS * kv->head_dim;
+  sp.page_indptr = kv->page_indptr;
+  sp.page_ids = kv->page_ids;
+  sp.seq_len = kv->seq_len;
+  sp.n_tuples = kv->n_tuples;
+  sp.n_layers = kv->n_layers;
+  sp.n_kv_heads = kv->n_kv_heads;
+  sp.gqa = kv->gqa_group;
+  sp.n_q = kv->n_q;
+  sp.n_ops = n_sel;
+  sp.rows_per_op = kv->gqa_group * kv->n_q;
+  sp.n_ops_total = n_ops_total;
+  sp.n_var_total = n_var_total;
+  int n_l = 1;
+  sp.n_var = n_vsel;
+  for (int i = 0; i < n_vsel; ++i) {
+    const ko_variant& v = variants[var_sel[i]];
+    sp.keep[i] = v.keep_permille;
+    sp.cut[i] = v.layer_cut;
+    sp.var_ids[i] = var_sel[i];
+    n_l = std::max(n_l, (int)v.layer_cut);
+  }
+  sp.n_l = n_l;
+  for (int i = 0; i < n_sel; ++i) {
+    const ko_operator& op = ops[op_sel[i]];
+    sp.op_ids[i] = op_sel[i];
+    sp.op_classes[i] = op.n_classes;
+    sp.bias[i] = op.b;
+    pp.q[i] = (const uint16_t*)op.q;
+    pp.w[i] = op.w;
+    pp.op_classes[i] = op.n_classes;
+  }
+  sp.qfrag = ws.qfrag;
+  sp.wfrag = ws.wfrag;
+  sp.part = ws.part;
+  sp.done = ws.done;
+  sp.unit_counter = ws.unit_counter;
+  sp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kv->head_dim));
+  pp.n_l = n_l;
+  pp.n_kv_heads = kv->n_kv_heads;
+  pp.gqa = kv->gqa_group;
+  pp.n_q = kv->n_q;
+  pp.n_layers = kv->n_layers;
+  pp.head_dim = kv->head_dim;
+  pp.n_ops = n_sel;
+  pp.rows_per_op = sp.rows_per_op;
+  pp.NH = NH;
+  pp.CPR = CPR;
+  pp.qfrag = ws.qfrag;
+  pp.wfrag = ws.wfrag;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ko_last_error(void) { return g_err.c_str(); }
+
+void ko_set_trace_events(void* ev_begin, void* ev_end) {
+  g_trace_begin = (cudaEvent_t)ev_begin;
+  g_trace_end = (cudaEvent_t)ev_end;
+}
+
+const char* ko_version(void) { return "ko 0.1 (sm_100a, mma.sync bf16 W-folded paged attention)"; }
+
+size_t ko_workspace_size(const ko_kv_cache* kv, const ko_operator* ops, int32_t n_ops,
+                         int32_t n_variants, int64_t n_work) {
+  if (validate_kv(kv) != KO_OK || validate_ops(kv, ops, n_ops) != KO_OK) return 0;
+  if (n_variants < 1 || n_variants > KO_MAX_VARIANTS || n_work < 0) return 0;
+  return layout(kv, max_classes(ops, n_ops), n_ops, n_variants, n_work, nullptr).total;
+}
+
+ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t n_ops,
+                         const ko_variant* variants, int32_t n_variants, const int32_t* tuple_idx,
+                         int64_t n_idx, float* margins, int32_t* classes, const ko_plan* plans,
+                         int32_t n_plans, const uint8_t* gold, int64_t* counts, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  ko_status st;
+  if ((st = validate_kv(kv)) != KO_OK) return st;
+  if ((st = validate_ops(kv, ops, n_ops)) != KO_OK) return st;
+  if ((st = validate_variants(kv, variants, n_variants)) != KO_OK) return st;
+  if (n_plans < 0 || n_plans > KO_MAX_PLANS) return fail(KO_EINVAL, "n_plans %d outside [0,64]", n_plans);
+  if (n_plans > 0 && !plans) return fail(KO_EINVAL, "plans is NULL with n_plans > 0");
+  int32_t ncls[KO_MAX_OPS] = {1, 1, 1, 1};
+  for (int o = 0; o < n_ops; ++o) ncls[o] = ops[o].n_classes;
+  for (int g = 0; g < n_plans; ++g)
+    if ((st = validate_plan(&plans[g], g, ncls, n_ops, n_variants)) != KO_OK) return st;
+  if (n_plans > 0 && !counts) return fail(KO_EINVAL, "counts is NULL with plans");
+  if (tuple_idx && n_idx < 0) return fail(KO_EINVAL, "n_idx < 0");
+  const bool routed = n_plans == 1;
+  if (!routed && !margins) return fail(KO_EINVAL, "margins may be NULL only in routed mode");
+  const int64_t n_work = tuple_idx ? n_idx : kv->n_tuples;
+  if (n_work > kv->n_tuples) return fail(KO_EINVAL, "n_idx > n_tuples");
+  const int maxc = max_classes(ops, n_ops);
+  if (!routed && (int64_t)n_ops * kv->gqa_group * kv->n_q > KO_MAX_ROWS)
+    return fail(KO_EUNSUPPORTED, "n_ops*gqa_group*n_q = %d > %d rows per kv-head",
+                n_ops * kv->gqa_group * kv->n_q, KO_MAX_ROWS);
+  if (!workspace) return fail(KO_EINVAL, "workspace is NULL");
+  if (((uintptr_t)workspace & 255) != 0) return fail(KO_EINVAL, "workspace not 256-byte aligned");
+  Workspace ws = layout(kv, maxc, n_ops, n_variants, n_work, (uint8_t*)workspace);
+  if (workspace_bytes < ws.total)
+    return fail(KO_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, ws.total);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_work == 0) return KO_OK;
+
+  if (!routed) {
+    // ---- grid / profiling mode: all ops × all variants in one read, every plan per tuple
+    int op_sel[KO_MAX_OPS], var_sel[KO_MAX_VARIANTS];
+    for (int i = 0; i < n_ops; ++i) op_sel[i] = i;
+    for (int i = 0; i < n_variants; ++i) var_sel[i] = i;
+    const int R = n_ops * kv->gqa_group * kv->n_q;
+    const int NH = R > 8 ? 2 : 1;
+    const int CPR = pow2_at_least(maxc);
+    ko::ScoreParams sp;
+    ko::PrepParams pp;
+    fill_common(sp, pp, kv, ops, op_sel, n_ops, variants, var_sel, n_variants, n_ops, n_variants,
+                ws, CPR, NH);
+    sp.work = tuple_idx;
+    sp.work_len_host = n_work;
+    sp.work_len_dev = nullptr;
+    sp.margins = margins;
+    sp.classes = classes;
+    sp.mode = ko::MODE_GRID;
+    sp.n_plans = n_plans;
+    sp.gold = gold;
+    sp.counts = (unsigned long long*)counts;
+    for (int g = 0; g < n_plans; ++g) sp.plans[g] = plans[g];
+    KO_CUDA(ko::launch_prep(pp, s));
+    KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
+    KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
+    if (g_trace_begin) KO_CUDA(cudaEventRecord(g_trace_begin, s));
+    KO_CUDA(ko::launch_score(sp, kv->head_dim, NH, CPR, n_work * sp.n_l * kv->n_kv_heads, s));
+    if (g_trace_end) KO_CUDA(cudaEventRecord(g_trace_end, s));
+    return KO_OK;
+  }
+
+  // ---- routed mode: the plan's stages in order; each stage scores only the tuples reaching it
+  const ko_plan& P = plans[0];
+  if (margins)
+    KO_CUDA(cudaMemsetAsync(margins, 0xFF, sizeof(float) * (size_t)n_ops * n_variants * kv->n_tuples, s));
+  KO_CUDA(ko::launch_route_init(ws.tuple_state, kv->n_tuples, s));
+  ko::RouteParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  rp.plan = P;
+  rp.n_ops = n_ops;
+  rp.n_variants = n_variants;
+  rp.n_tuples = kv->n_tuples;
+  for (int o = 0; o < n_ops; ++o) rp.n_classes[o] = ops[o].n_classes;
+  rp.subset = tuple_idx;
+  rp.n_subset = n_work;
+  rp.tuple_state = ws.tuple_state;
+  rp.worklist = ws.worklist;
+  rp.worklist_len = ws.worklist_len;
+  rp.gold = gold;
+  rp.counts = (unsigned long long*)counts;
+  for (int s_i = 0; s_i < P.n_stages; ++s_i) {
+    const ko_stage& stg = P.stage[s_i];
+    rp.stage = s_i;
+    KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));  // unit counter + worklist length
+    KO_CUDA(ko::launch_route_reach(rp, s));
+    int op_sel[1] = {stg.op}, var_sel[1] = {stg.variant};
+    const int R = kv->gqa_group * kv->n_q;
+    const int NH = R > 8 ? 2 : 1;
+    const int CPR = pow2_at_least(ops[stg.op].n_classes);
+    ko::ScoreParams sp;
+    ko::PrepParams pp;
+    fill_common(sp, pp, kv, ops, op_sel, 1, variants, var_sel, 1, n_ops, n_variants, ws, CPR, NH);
+    sp.work = ws.worklist;
+    sp.work_len_host = 0;
+    sp.work_len_dev = (const int64_t*)ws.worklist_len;
+    sp.margins = margins;
+    sp.classes = classes;
+    sp.mode = ko::MODE_STAGE;
+    sp.n_plans = 1;
+    sp.plans[0] = P;
+    sp.stage_idx = s_i;
+    sp.tuple_state = ws.tuple_state;
+    sp.counts = (unsigned long long*)counts;
+    KO_CUDA(ko::launch_prep(pp, s));
+    KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
+    if (g_trace_begin && s_i == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
+    KO_CUDA(ko::launch_score(sp, kv->head_dim, NH, CPR, n_work * sp.n_l * kv->n_kv_heads, s));
+    if (g_trace_end && s_i + 1 == P.n_stages) KO_CUDA(cudaEventRecord(g_trace_end, s));
+  }
+  KO_CUDA(ko::launch_final_counts(rp, s));
+  return KO_OK;
+}
+
+ko_status ko_route(const ko_plan* plan, const float* margins, const int32_t* classes,
+                   const int32_t* n_classes, int32_t n_ops, int32_t n_variants, int64_t n_tuples,
+                   int32_t stage, uint32_t* tuple_state, int32_t* worklist_out,
+                   int64_t* worklist_len, const uint8_t* gold, int64_t* counts, void* stream) {
+  if (!plan || !margins || !n_classes || !tuple_state || !counts)
+    return fail(KO_EINVAL, "ko_route: NULL plan/margins/n_classes/tuple_state/counts");
+  if (n_ops < 1 || n_ops > KO_MAX_OPS) return fail(KO_EINVAL, "n_ops %d", n_ops);
+  if (n_variants < 1 || n_variants > KO_MAX_VARIANTS) return fail(KO_EINVAL, "n_variants %d", n_variants);
+  if (n_tuples < 0 || n_tuples > 0x7fffffffll) return fail(KO_EINVAL, "n_tuples %lld", (long long)n_tuples);
+  for (int o = 0; o < n_ops; ++o)
+    if (n_classes[o] < 1 || n_classes[o] > KO_MAX_CLASSES) return fail(KO_EINVAL, "n_classes[%d]", o);
+  ko_status st;
+  if ((st = validate_plan(plan, 0, n_classes, n_ops, n_variants)) != KO_OK) return st;
+  if (stage < -1 || stage >= plan->n_stages) return fail(KO_EINVAL, "stage %d", stage);
+  bool has_map = false;
+  for (int s = 0; s < plan->n_stages; ++s) has_map |= n_classes[plan->stage[s].op] > 1;
+  if (has_map && !classes) return fail(KO_EINVAL, "classes required for map operators");
+  if ((worklist_out == nullptr) != (worklist_len == nullptr))
+    return fail(KO_EINVAL, "worklist_out and worklist_len must both be set or both NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  ko::RouteParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  rp.plan = *plan;
+  rp.margins = margins;
+  rp.classes = classes;
+  for (int o = 0; o < n_ops; ++o) rp.n_classes[o] = n_classes[o];
+  rp.n_ops = n_ops;
+  rp.n_variants = n_variants;
+  rp.n_tuples = n_tuples;
+  rp.tuple_state = tuple_state;
+  rp.worklist = worklist_out;
+  rp.worklist_len = (unsigned long long*)worklist_len;
+  rp.gold = gold;
+  rp.counts = (unsigned long long*)counts;
+  if (n_tuples == 0) {
+    if (worklist_len) KO_CUDA(cudaMemsetAsync(worklist_len, 0, 8, s));
+    return KO_OK;
+  }
+  if (worklist_len) KO_CUDA(cudaMemsetAsync(worklist_len, 0, 8, s));
+  if (stage == -1) {
+    KO_CUDA(ko::launch_route_plan(rp, s));
+    return KO_OK;
+  }
+  rp.stage = stage;
+  KO_CUDA(ko::launch_route_apply(rp, s));
+  if (worklist_out) {
+    rp.stage = stage + 1;  // tuples reaching the next stage (none after the last)
+    KO_CUDA(ko::launch_route_reach(rp, s));
+  }
+  return KO_OK;
+}
+
+ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* margins,
+                          const int32_t* classes, const int32_t* n_classes, int32_t n_ops,
+                          int32_t n_variants, int64_t n_tuples, const uint8_t* gold,
+                          int64_t* counts, void* stream) {
+  if (!plans || !margins || !n_classes || !counts)
+    return fail(KO_EINVAL, "ko_reduce_stats: NULL plans/margins/n_classes/counts");
+  if (n_plans < 1 || n_plans > KO_MAX_PLANS) return fail(KO_EINVAL, "n_plans %d", n_plans);
+  if (n_ops < 1 || n_ops > KO_MAX_OPS) return fail(KO_EINVAL, "n_ops %d", n_ops);
+  if (n_variants < 1 || n_variants > KO_MAX_VARIANTS) return fail(KO_EINVAL, "n_variants %d", n_variants);
+  if (n_tuples < 0) return fail(KO_EINVAL, "n_tuples < 0");
+  for (int o = 0; o < n_ops; ++o)
+    if (n_classes[o] < 1 || n_classes[o] > KO_MAX_CLASSES) return fail(KO_EINVAL, "n_classes[%d]", o);
+  ko_status st;
+  bool has_map = false;
+  for (int g = 0; g < n_plans; ++g) {
+    if ((st = validate_plan(&plans[g], g, n_classes, n_ops, n_variants)) != KO_OK) return st;
+    for (int s = 0; s < plans[g].n_stages; ++s) has_map |= n_classes[plans[g].stage[s].op] > 1;
+  }
+  if (has_map && !classes) return fail(KO_EINVAL, "classes required for map operators");
+  if (n_tuples == 0) return KO_OK;
+  ko::ReduceParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  rp.n_plans = n_plans;
+  rp.margins = margins;
+  rp.classes = classes;
+  for (int o = 0; o < n_ops; ++o) rp.n_classes[o] = n_classes[o];
+  rp.n_ops = n_ops;
+  rp.n_variants = n_variants;
+  rp.n_tuples = n_tuples;
+  rp.gold = gold;
+  rp.counts = (unsigned long long*)counts;
+  for (int g = 0; g < n_plans; ++g) rp.plans[g] = plans[g];
+  KO_CUDA(ko::launch_reduce(rp, (cudaStream_t)stream));
+  return KO_OK;
+}
+
+// ---- Bayesian lower bound (host): I^{-1}(1 − α; 1 + a, 1 + b) -------------------------------
+// Regularized incomplete beta by the continued fraction (modified Lentz), inverse by bisection.
+static double betacf(double a, double b, double x) {
+  const double tiny = 1e-300, eps = 1e-16;
+  double qab = a + b, qap = a + 1.0, qam = a - 1.0;
+  double c = 1.0, d = 1.0 - qab * x / qap;
+  if (std::fabs(d) < tiny) d = tiny;
+  d = 1.0 / d;
+  double h = d;
+  for (int m = 1; m <= 100000; ++m) {
+    const int m2 = 2 * m;
+    double aa = m * (b - m) * x / ((qam + m2) * (a + m2));
+    d = 1.0 + aa * d; if (std::fabs(d) < tiny) d = tiny;
+    c = 1.0 + aa / c; if (std::fabs(c) < tiny) c = tiny;
+    d = 1.0 / d; h *= d * c;
+    aa = -(a + m) * (qab + m) * x / ((a + m2) * (qap + m2));
+    d = 1.0 + aa * d; if (std::fabs(d) < tiny) d = tiny;
+    c = 1.0 + aa / c; if (std::fabs(c) < tiny) c = tiny;
+    d = 1.0 / d;
+    const double del = d * c;
+    h *= del;
+    if (std::fabs(del - 1.0) < eps) break;
+  }
+  return h;
+}
+
+static double betainc_reg(double a, double b, double x) {
+  if (x <= 0.0) return 0.0;
+  if (x >= 1.0) return 1.0;
+  const double lbt = std::lgamma(a + b) - std::lgamma(a) - std::lgamma(b) + a * std::log(x) +
+                     b * std::log1p(-x);
+  if (x < (a + 1.0) / (a + b + 2.0)) return std::exp(lbt) * betacf(a, b, x) / a;
+  return 1.0 - std::exp(lbt) * betacf(b, a, 1.0 - x) / b;
+}
+
+double ko_beta_lower_bound(int64_t a_cnt, int64_t b_cnt, double alpha) {
+  if (a_cnt < 0 || b_cnt < 0 || !(alpha > 0.0 && alpha < 1.0)) return NAN;
+  const double a = 1.0 + (double)a_cnt, b = 1.0 + (double)b_cnt, target = 1.0 - alpha;
+  double lo = 0.0, hi = 1.0;
+  for (int it = 0; it < 200 && hi - lo > 1e-16; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (betainc_reg(a, b, mid) < target) lo = mid; else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+}  // extern "C"

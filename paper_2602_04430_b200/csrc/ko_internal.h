@@ -1,0 +1,121 @@
+// ko_internal.h — host-side contract between ko_api.cpp (validation, workspace, dispatch) and
+// ko_kernels.cu (device code + launchers).  Not part of the public ABI (that is include/ko.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "ko.h"
+
+namespace ko {
+
+constexpr int kMaxOps = KO_MAX_OPS;
+constexpr int kMaxVar = KO_MAX_VARIANTS;
+constexpr int kMaxCls = KO_MAX_CLASSES;
+constexpr int kMaxPlans = KO_MAX_PLANS;
+constexpr int kCountsPerPlan = KO_COUNTS_PER_PLAN;
+constexpr int kThreads = 128;  // score kernel CTA size (4 warps, one work unit per warp)
+
+enum Mode : int32_t { MODE_GRID = 0, MODE_STAGE = 1 };
+
+// One launch of the scoring kernel.  "Local" op/variant indices are positions in this launch;
+// op_ids / var_ids map them to the caller's indices (margins layout, plans, gold).
+struct ScoreParams {
+  // paged KV store
+  const uint16_t* pool;
+  int64_t page_elems;  // bf16 elements per page = n_layers*2*n_kv_heads*16*head_dim
+  const int64_t* page_indptr;
+  const int32_t* page_ids;
+  const int32_t* seq_len;
+  int64_t n_tuples;
+  int32_t n_layers, n_kv_heads, gqa, n_q;
+  // work list (tuple ids); NULL = identity.  Length from work_len_dev if non-NULL.
+  const int32_t* work;
+  int64_t work_len_host;
+  const int64_t* work_len_dev;
+  int32_t n_l;  // layers computed = max layer_cut over this launch's variants
+  // operators of this launch
+  int32_t n_ops;
+  int32_t op_ids[kMaxOps];
+  int32_t op_classes[kMaxOps];
+  const float* bias[kMaxOps];  // device fp32 [n_classes] per op
+  int32_t rows_per_op;  // gqa * n_q
+  int32_t n_ops_total, n_var_total;
+  // variants of this launch
+  int32_t n_var;
+  int32_t keep[kMaxVar], cut[kMaxVar], var_ids[kMaxVar];
+  // prepared tensor-core fragments (workspace)
+  const uint4* qfrag;  // [n_l*Hkv][KS][32]
+  const uint4* wfrag;  // [n_l*Hkv][NT][KS][32]
+  // scratch (workspace)
+  float* part;                     // [n_work][n_l*Hkv][n_ops][n_var][CPR]
+  int32_t* done;                   // [n_work]
+  unsigned long long* unit_counter;
+  // outputs
+  float* margins;   // [n_ops_total][n_var_total][n_tuples] or NULL
+  int32_t* classes;  // same or NULL
+  float scale_log2;  // log2(e)/sqrt(head_dim)
+  // grid mode: per-tuple evaluation of every plan (indices are caller's = local here)
+  int32_t mode;
+  int32_t n_plans;
+  const uint8_t* gold;  // [n_ops_total][n_tuples] or NULL
+  unsigned long long* counts;  // [n_plans][kCountsPerPlan] (int64 bit pattern)
+  // stage mode: apply plan stage `stage_idx` of `plan` (routed execution)
+  int32_t stage_idx;
+  uint32_t* tuple_state;
+  ko_plan plans[kMaxPlans];
+};
+
+struct PrepParams {
+  int32_t n_l, n_kv_heads, gqa, n_q, n_layers, head_dim;
+  int32_t n_ops, rows_per_op, NH, CPR;
+  const uint16_t* q[kMaxOps];
+  const float* w[kMaxOps];
+  int32_t op_classes[kMaxOps];
+  uint4* qfrag;
+  uint4* wfrag;
+};
+
+struct RouteParams {
+  ko_plan plan;
+  const float* margins;
+  const int32_t* classes;
+  int32_t n_classes[kMaxOps];
+  int32_t n_ops, n_variants;
+  int64_t n_tuples;
+  const int32_t* subset;  // optional tuple subset (NULL = all)
+  int64_t n_subset;
+  int32_t stage;
+  uint32_t* tuple_state;
+  int32_t* worklist;
+  unsigned long long* worklist_len;
+  const uint8_t* gold;
+  unsigned long long* counts;
+};
+
+struct ReduceParams {
+  int32_t n_plans;
+  const float* margins;
+  const int32_t* classes;
+  int32_t n_classes[kMaxOps];
+  int32_t n_ops, n_variants;
+  int64_t n_tuples;
+  const uint8_t* gold;
+  unsigned long long* counts;
+  ko_plan plans[kMaxPlans];
+};
+
+// launchers (ko_kernels.cu); return cudaSuccess or the launch error
+cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
+cudaError_t launch_score(const ScoreParams& p, int head_dim, int NH, int CPR, int64_t max_units,
+                         cudaStream_t s);
+cudaError_t launch_route_reach(const RouteParams& p, cudaStream_t s);  // build worklist for stage
+cudaError_t launch_route_apply(const RouteParams& p, cudaStream_t s);  // apply stage on margins
+cudaError_t launch_route_plan(const RouteParams& p, cudaStream_t s);   // whole plan on margins
+cudaError_t launch_route_init(uint32_t* state, int64_t n, cudaStream_t s);
+cudaError_t launch_final_counts(const RouteParams& p, cudaStream_t s);  // TP/FP/FN from state
+cudaError_t launch_reduce(const ReduceParams& p, cudaStream_t s);
+cudaError_t launch_fill_f32(float* p, float v, int64_t n, cudaStream_t s);
+
+}  // namespace ko

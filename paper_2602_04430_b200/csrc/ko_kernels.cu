@@ -1,0 +1,798 @@
+// ko_kernels.cu — sm_100a kernels of the KV-cache semantic-operator scoring pass.
+//
+// Hot kernel: ko_score_kernel<D, NH, CPR>.  One warp owns one work unit = (tuple t, layer l,
+// kv-head h) and streams that unit's K and V rows (importance order, page by page) straight from
+// HBM with 128-bit non-allocating loads, one page ahead.  Per 16-token page:
+//   S = Q · Kᵀ        on tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate): the rows
+//                     attending kv-head h (n_ops · gqa · n_q ≤ 16) are the M dimension, the
+//                     page's tokens the N dimension, head_dim the K dimension;
+//   U = W · Vᵀ        same shape: the readout W of every row/class is folded through V, so the
+//                     logit contribution of a row is Σ_i softmax_i · U_i (linearity of
+//                     z = b + W·O, DESIGN.md §"Kernel").  W is fp32 and enters as bf16 hi + lo
+//                     (rows 0-7 / 8-15 of the same MMA);
+//   online softmax    lane-local running (max, sum, Σ p·u) per row over the lane's own tokens,
+//                     merged across the 4 lanes of a quad only at variant snapshots;
+//   snapshots         tokens are in importance order, so every keep ratio is a prefix: the
+//                     state is snapshot when the token index reaches each variant's n_kept, so
+//                     one read serves every variant (nested prefixes, Q2); layer cuts select
+//                     which units a variant sums.
+// Partial logits per (unit, op, variant, class) go to a workspace; the warp that completes a
+// tuple's last unit sums them in a FIXED order (bitwise-deterministic margins), derives margin
+// and class, then either evaluates every plan of the grid (grid mode) or applies one cascade stage
+// (stage mode), counting with shared-memory integer atomics flushed once per CTA.
+//
+// The key/value data layout, the d-permutation that lets one LDG.128 feed two MMA k-steps, and
+// the roofline are in DESIGN.md §"Kernel".
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "ko_internal.h"
+
+namespace ko {
+namespace {
+
+enum { D_ACCEPT = 0, D_REJECT = 1, D_UNSURE = 2, D_RESOLVED = 3 };
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t a0, const uint32_t a1,
+                                         const uint32_t a2, const uint32_t a3, const uint32_t b0,
+                                         const uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const uint16_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ int n_kept(int L, int keep) {  // Q3: max(1, floor(L·keep/1000))
+  int n = (int)(((long long)L * keep) / 1000);
+  return n < 1 ? 1 : n;
+}
+
+// Step-5 decision; identical semantics to the oracle (strict inequalities, Q5/Q6/Q13).
+__device__ __forceinline__ int decide(float m, const ko_stage& st, int ncls) {
+  if (ncls <= 1) {
+    if (st.is_final) return m > st.theta_hi ? D_ACCEPT : D_REJECT;
+    if (m > st.theta_hi) return D_ACCEPT;
+    if (m < st.theta_lo) return D_REJECT;
+    return D_UNSURE;
+  }
+  if (st.is_final) return D_RESOLVED;
+  return m > st.theta_hi ? D_RESOLVED : D_UNSURE;
+}
+
+__device__ __forceinline__ int op_status(uint32_t st, int o) { return (st >> (1 + 2 * o)) & 3; }
+
+// Whole-plan evaluation for one tuple (Eqs. accept-i/reject-i/unsure-i, conjunctive
+// inter-op semantics P:536-539, counts P:350-352).  ms/cs: margins/classes indexed
+// [op * n_var + variant].  cnt: this plan's int32 counter row (shared memory).
+// Returns the final tuple state (bit0 alive, 2-bit status per op, 4-bit class per op).
+__device__ uint32_t eval_plan(const ko_plan& P, const float* ms, const int32_t* cs, int n_var,
+                              const int32_t* ncls, const uint8_t* gold, int64_t n_tuples,
+                              int64_t t, int* cnt) {
+  uint32_t state = 1u;
+  uint32_t referenced = 0;
+  for (int s = 0; s < P.n_stages; ++s) referenced |= 1u << P.stage[s].op;
+  for (int s = 0; s < P.n_stages; ++s) {
+    const ko_stage& st = P.stage[s];
+    const int o = st.op;
+    if (!(state & 1u) || op_status(state, o) != 0) continue;
+    if (cnt) atomicAdd(&cnt[5 + 4 * s], 1);
+    const int idx = o * n_var + st.variant;
+    const int d = decide(ms[idx], st, ncls[o]);
+    if (d == D_ACCEPT || d == D_RESOLVED) {
+      state |= 1u << (1 + 2 * o);
+      if (d == D_RESOLVED) state |= ((uint32_t)cs[idx] & 15u) << (16 + 4 * o);
+      if (cnt) atomicAdd(&cnt[6 + 4 * s], 1);
+    } else if (d == D_REJECT) {
+      state &= ~1u;
+      state |= 2u << (1 + 2 * o);
+      if (cnt) atomicAdd(&cnt[7 + 4 * s], 1);
+    } else {
+      if (cnt) atomicAdd(&cnt[8 + 4 * s], 1);
+    }
+  }
+  if (cnt) {
+    const bool in_out = state & 1u;
+    bool in_gold = gold != nullptr, maps_ok = true;
+    if (gold) {
+      for (int o = 0; o < kMaxOps; ++o) {
+        if (!(referenced & (1u << o))) continue;
+        const uint8_t gv = gold[(int64_t)o * n_tuples + t];
+        if (ncls[o] <= 1) {
+          if (gv != 1) in_gold = false;
+        } else if (((state >> (16 + 4 * o)) & 15u) != gv || op_status(state, o) != 1) {
+          maps_ok = false;
+        }
+      }
+    }
+    if (in_out) atomicAdd(&cnt[KO_C_OUT], 1);
+    if (in_gold) atomicAdd(&cnt[KO_C_GOLD], 1);
+    if (in_out && in_gold && maps_ok) atomicAdd(&cnt[KO_C_TP], 1);
+  }
+  return state;
+}
+
+// Flush per-CTA int32 counters (FP/FN derived from n_out/n_gold/TP) into the int64 output.
+__device__ void flush_counts(int* s_cnt, int n_rows, unsigned long long* counts) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_rows * kCountsPerPlan; i += blockDim.x) {
+    const int k = i % kCountsPerPlan;
+    const int* row = s_cnt + (i - k);
+    long long v = s_cnt[i];
+    if (k == KO_C_FP) v = (long long)row[KO_C_OUT] - row[KO_C_TP];
+    if (k == KO_C_FN) v = (long long)row[KO_C_GOLD] - row[KO_C_TP];
+    if (v) atomicAdd(&counts[i], (unsigned long long)v);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// The scoring kernel
+// ------------------------------------------------------------------------------------------
+template <int KP>
+struct PageRegs {
+  uint4 k[2][KP];
+  uint4 v[2][KP];
+};
+
+template <int D, int NH, int CPR>
+__global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_constant__ ScoreParams p) {
+  constexpr int KS = D / 16;  // mma k-steps over head_dim
+  constexpr int KP = D / 32;  // 128-bit loads per token row per lane (each feeds 2 k-steps)
+  constexpr int NT = NH * CPR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+
+  __shared__ int s_cnt[kMaxPlans * kCountsPerPlan];
+  __shared__ float s_z[kThreads / 32][kMaxOps * kMaxVar * kMaxCls];
+  __shared__ float s_m[kThreads / 32][kMaxOps * kMaxVar];
+  __shared__ int32_t s_c[kThreads / 32][kMaxOps * kMaxVar];
+
+  const int n_cnt_rows = p.mode == MODE_GRID ? p.n_plans : (p.tuple_state ? 1 : 0);
+  for (int i = threadIdx.x; i < n_cnt_rows * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+
+  const int64_t n_work = p.work_len_dev ? *p.work_len_dev : p.work_len_host;
+  const int Hkv = p.n_kv_heads;
+  const int upt = p.n_l * Hkv;  // units per tuple
+  const int64_t n_units = n_work * upt;
+  const int R = p.n_ops * p.rows_per_op;
+  const int64_t kv_stride = (int64_t)Hkv * 16 * D;  // K block → V block
+
+  // row slot → local op for this lane's two half-slots
+  int slot_op[NH];
+#pragma unroll
+  for (int hs = 0; hs < NH; ++hs) {
+    const int rho = hs * 8 + g;
+    slot_op[hs] = rho < R ? rho / p.rows_per_op : -1;
+  }
+
+  for (;;) {
+    long long u = 0;
+    if (lane == 0) u = (long long)atomicAdd(p.unit_counter, 1ull);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= n_units) break;
+    const int64_t wslot = u / upt;
+    const int unit = (int)(u - wslot * upt);
+    const int l = unit / Hkv, h = unit - (unit / Hkv) * Hkv;
+    const int64_t t = p.work ? (int64_t)p.work[wslot] : wslot;
+    const int L = p.seq_len[t];
+
+    // tokens this unit must stream: the largest prefix among variants whose cut includes l
+    int n_need = 0;
+    for (int v = 0; v < p.n_var; ++v)
+      if (p.cut[v] > l) n_need = max(n_need, n_kept(L, p.keep[v]));
+    int next_snap = n_need;  // smallest active n_kept (first snapshot point)
+    for (int v = 0; v < p.n_var; ++v)
+      if (p.cut[v] > l) next_snap = min(next_snap, n_kept(L, p.keep[v]));
+
+    // operator-query fragments for (l, h)
+    const int lh = l * Hkv + h;
+    uint32_t qa[KS][4];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint4 f = __ldg(p.qfrag + ((size_t)lh * KS + ks) * 32 + lane);
+      qa[ks][0] = f.x; qa[ks][1] = f.y; qa[ks][2] = f.z; qa[ks][3] = f.w;
+    }
+    uint32_t wa1[NT == 1 ? KS : 1][4];
+    if constexpr (NT == 1) {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const uint4 f = __ldg(p.wfrag + ((size_t)lh * KS + ks) * 32 + lane);
+        wa1[ks][0] = f.x; wa1[ks][1] = f.y; wa1[ks][2] = f.z; wa1[ks][3] = f.w;
+      }
+    }
+    const uint4* wbase = p.wfrag + (size_t)lh * NT * KS * 32 + lane;
+
+    // lane-local online-softmax state per half-slot (log2 domain)
+    float mx[NH], sm[NH], ac[NH][CPR];
+#pragma unroll
+    for (int hs = 0; hs < NH; ++hs) {
+      mx[hs] = -CUDART_INF_F;
+      sm[hs] = 0.f;
+#pragma unroll
+      for (int c = 0; c < CPR; ++c) ac[hs][c] = 0.f;
+    }
+
+    const int64_t pbase = p.page_indptr[t];
+    const int n_pages = (n_need + 15) >> 4;
+    const size_t koff = ((size_t)(l * 2) * Hkv + h) * 16 * D;
+    int pid_chunk = -1;
+    int pid_reg = 0;
+
+    auto page_id = [&](int pg) -> int64_t {
+      const int chunk = pg >> 5;
+      if (chunk != pid_chunk) {
+        const int idx = (chunk << 5) + lane;
+        pid_reg = idx < n_pages ? __ldg(p.page_ids + pbase + idx) : 0;
+        pid_chunk = chunk;
+      }
+      return (int64_t)__shfl_sync(0xffffffffu, pid_reg, pg & 31);
+    };
+
+    auto load_page = [&](PageRegs<KP>& r, int pg) {
+      const uint16_t* kb = p.pool + page_id(pg) * p.page_elems + koff;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int tok = nt * 8 + g;
+        const bool valid = (pg * 16 + tok) < n_need;
+        const uint16_t* kr = kb + tok * D + 8 * q;
+#pragma unroll
+        for (int j = 0; j < KP; ++j) {
+          r.k[nt][j] = valid ? ldg_stream(kr + 32 * j) : make_uint4(0, 0, 0, 0);
+          r.v[nt][j] = valid ? ldg_stream(kr + kv_stride + 32 * j) : make_uint4(0, 0, 0, 0);
+        }
+      }
+    };
+
+    int snap_lo = 0;  // first token not yet folded into the running state
+
+    auto process_page = [&](const PageRegs<KP>& r, int pg) {
+      // ---- tensor cores: S = Q·Kᵀ and U = W·Vᵀ for this page's 16 tokens
+      float S[2][4];
+      float U[NT][2][4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) S[nt][i] = 0.f;
+#pragma unroll
+        for (int tt = 0; tt < NT; ++tt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) U[tt][nt][i] = 0.f;
+#pragma unroll
+        for (int j = 0; j < KP; ++j) {
+          mma16816(S[nt], qa[2 * j][0], qa[2 * j][1], qa[2 * j][2], qa[2 * j][3], r.k[nt][j].x,
+                   r.k[nt][j].y);
+          mma16816(S[nt], qa[2 * j + 1][0], qa[2 * j + 1][1], qa[2 * j + 1][2], qa[2 * j + 1][3],
+                   r.k[nt][j].z, r.k[nt][j].w);
+        }
+#pragma unroll
+        for (int tt = 0; tt < NT; ++tt) {
+#pragma unroll
+          for (int j = 0; j < KP; ++j) {
+            uint32_t a0[4], a1[4];
+            if constexpr (NT == 1) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) { a0[i] = wa1[2 * j][i]; a1[i] = wa1[2 * j + 1][i]; }
+            } else {
+              const uint4 f0 = __ldg(wbase + ((size_t)tt * KS + 2 * j) * 32);
+              const uint4 f1 = __ldg(wbase + ((size_t)tt * KS + 2 * j + 1) * 32);
+              a0[0] = f0.x; a0[1] = f0.y; a0[2] = f0.z; a0[3] = f0.w;
+              a1[0] = f1.x; a1[1] = f1.y; a1[2] = f1.z; a1[3] = f1.w;
+            }
+            mma16816(U[tt][nt], a0[0], a0[1], a0[2], a0[3], r.v[nt][j].x, r.v[nt][j].y);
+            mma16816(U[tt][nt], a1[0], a1[1], a1[2], a1[3], r.v[nt][j].z, r.v[nt][j].w);
+          }
+        }
+      }
+      // ---- per-lane token indices and values: k = nt*2 + e ↔ token pg*16 + nt*8 + 2q + e
+      const int page_hi = min(pg * 16 + 16, n_need);
+      for (;;) {
+        const int seg_hi = min(next_snap, page_hi);
+        // fold tokens [snap_lo, seg_hi) of this page into the lane-local state
+#pragma unroll
+        for (int hs = 0; hs < NH; ++hs) {
+          float x[4];
+          float xm = -CUDART_INF_F;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int nt = k >> 1, e = k & 1;
+            const int tok = pg * 16 + nt * 8 + 2 * q + e;
+            const bool in = tok >= snap_lo && tok < seg_hi;
+            x[k] = in ? S[nt][2 * hs + e] * p.scale_log2 : -CUDART_INF_F;
+            xm = fmaxf(xm, x[k]);
+          }
+          const float mn = fmaxf(mx[hs], xm);
+          if (mn != -CUDART_INF_F) {
+            const float corr = ex2(mx[hs] - mn);
+            float ps[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ps[k] = ex2(x[k] - mn);
+            sm[hs] = sm[hs] * corr + ((ps[0] + ps[1]) + (ps[2] + ps[3]));
+#pragma unroll
+            for (int c = 0; c < CPR; ++c) {
+              const int tt = hs * CPR + c;
+              float a = ac[hs][c] * corr;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int nt = k >> 1, e = k & 1;
+                a = fmaf(ps[k], U[tt][nt][e] + U[tt][nt][2 + e], a);
+              }
+              ac[hs][c] = a;
+            }
+            mx[hs] = mn;
+          }
+        }
+        snap_lo = seg_hi;
+        if (seg_hi == next_snap) {
+          // ---- snapshot: merge the quad's lane states, reduce rows per op, emit partials
+          float val[NH][CPR];
+#pragma unroll
+          for (int hs = 0; hs < NH; ++hs) {
+            float M = mx[hs];
+            M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
+            M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
+            const float f = mx[hs] == -CUDART_INF_F ? 0.f : ex2(mx[hs] - M);
+            float den = sm[hs] * f;
+            den += __shfl_xor_sync(0xffffffffu, den, 1);
+            den += __shfl_xor_sync(0xffffffffu, den, 2);
+#pragma unroll
+            for (int c = 0; c < CPR; ++c) {
+              float a = ac[hs][c] * f;
+              a += __shfl_xor_sync(0xffffffffu, a, 1);
+              a += __shfl_xor_sync(0xffffffffu, a, 2);
+              val[hs][c] = __fdiv_rn(a, den);
+            }
+          }
+          float opv[kMaxOps][CPR];
+#pragma unroll
+          for (int o = 0; o < kMaxOps; ++o) {
+#pragma unroll
+            for (int c = 0; c < CPR; ++c) {
+              float x = 0.f;
+#pragma unroll
+              for (int hs = 0; hs < NH; ++hs) x += slot_op[hs] == o ? val[hs][c] : 0.f;
+              if (o < p.n_ops) {
+                x += __shfl_xor_sync(0xffffffffu, x, 4);
+                x += __shfl_xor_sync(0xffffffffu, x, 8);
+                x += __shfl_xor_sync(0xffffffffu, x, 16);
+              }
+              opv[o][c] = x;
+            }
+          }
+          if (lane == 0) {
+            for (int v = 0; v < p.n_var; ++v) {
+              if (!(p.cut[v] > l) || n_kept(L, p.keep[v]) != next_snap) continue;
+#pragma unroll
+              for (int o = 0; o < kMaxOps; ++o) {
+                if (o >= p.n_ops) break;
+                float* dst = p.part + ((((size_t)wslot * upt + unit) * p.n_ops + o) * p.n_var + v) * CPR;
+#pragma unroll
+                for (int c = 0; c < CPR; ++c) dst[c] = opv[o][c];
+              }
+            }
+          }
+          // advance to the next larger snapshot point
+          int nxt = 0x7fffffff;
+          for (int v = 0; v < p.n_var; ++v)
+            if (p.cut[v] > l) {
+              const int nk = n_kept(L, p.keep[v]);
+              if (nk > next_snap) nxt = min(nxt, nk);
+            }
+          next_snap = nxt;
+        }
+        if (snap_lo >= page_hi) break;
+      }
+    };
+
+    // ---- page loop, one page of loads in flight ahead of the math
+    PageRegs<KP> ra, rb;
+    load_page(ra, 0);
+    for (int pg = 0; pg < n_pages; pg += 2) {
+      if (pg + 1 < n_pages) load_page(rb, pg + 1);
+      process_page(ra, pg);
+      if (pg + 1 >= n_pages) break;
+      if (pg + 2 < n_pages) load_page(ra, pg + 2);
+      process_page(rb, pg + 1);
+    }
+
+    // ---- tuple completion: the warp finishing the tuple's last unit finalises it
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(p.done + wslot, 1) == upt - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) continue;
+    __threadfence();
+
+    float* zs = s_z[warp];
+    const int nz = p.n_ops * p.n_var * CPR;
+    for (int idx = lane; idx < nz; idx += 32) {
+      const int c = idx % CPR;
+      const int v = (idx / CPR) % p.n_var;
+      const int o = idx / (CPR * p.n_var);
+      float zf = -CUDART_INF_F;
+      if (c < p.op_classes[o]) {
+        double z = (double)__ldg(p.bias[o] + c);
+        const float* src = p.part + ((size_t)wslot * upt * p.n_ops + o) * p.n_var * CPR + v * CPR + c;
+        const size_t ustride = (size_t)p.n_ops * p.n_var * CPR;
+        const int u_end = min(p.cut[v], p.n_l) * Hkv;  // units are l-major: l < cut ⇔ u < cut·Hkv
+        for (int uu = 0; uu < u_end; ++uu) z += (double)__ldcg(src + uu * ustride);
+        zf = (float)z;
+      }
+      zs[idx] = zf;
+    }
+    __syncwarp();
+    for (int idx = lane; idx < p.n_ops * p.n_var; idx += 32) {
+      const int o = idx / p.n_var, v = idx % p.n_var;
+      const float* zz = zs + idx * CPR;
+      float m;
+      int cls = 0;
+      if (p.op_classes[o] <= 1) {
+        m = zz[0];
+      } else {
+        for (int c = 1; c < p.op_classes[o]; ++c)
+          if (zz[c] > zz[cls]) cls = c;  // lowest index on ties
+        float second = -CUDART_INF_F;
+        for (int c = 0; c < p.op_classes[o]; ++c)
+          if (c != cls && zz[c] > second) second = zz[c];
+        m = zz[cls] - second;
+      }
+      const size_t oi = ((size_t)p.op_ids[o] * p.n_var_total + p.var_ids[v]) * p.n_tuples + t;
+      if (p.margins) p.margins[oi] = m;
+      if (p.classes) p.classes[oi] = cls;
+      s_m[warp][idx] = m;
+      s_c[warp][idx] = cls;
+    }
+    __syncwarp();
+    if (p.mode == MODE_GRID) {
+      for (int gp = lane; gp < p.n_plans; gp += 32)
+        eval_plan(p.plans[gp], s_m[warp], s_c[warp], p.n_var, p.op_classes, p.gold, p.n_tuples, t,
+                  s_cnt + gp * kCountsPerPlan);
+    } else if (lane == 0 && p.tuple_state) {
+      // routed execution: apply stage `stage_idx` (this launch has exactly its op and variant)
+      const ko_stage& st = p.plans[0].stage[p.stage_idx];
+      const int o = st.op;
+      const int d = decide(s_m[warp][0], st, p.op_classes[0]);
+      uint32_t state = p.tuple_state[t];
+      int* cnt = s_cnt + 5 + 4 * p.stage_idx;
+      atomicAdd(&cnt[0], 1);
+      if (d == D_ACCEPT || d == D_RESOLVED) {
+        state |= 1u << (1 + 2 * o);
+        if (d == D_RESOLVED) state |= ((uint32_t)s_c[warp][0] & 15u) << (16 + 4 * o);
+        atomicAdd(&cnt[1], 1);
+      } else if (d == D_REJECT) {
+        state = (state & ~1u) | (2u << (1 + 2 * o));
+        atomicAdd(&cnt[2], 1);
+      } else {
+        atomicAdd(&cnt[3], 1);
+      }
+      p.tuple_state[t] = state;
+    }
+  }
+  if (n_cnt_rows) flush_counts(s_cnt, n_cnt_rows, p.counts);
+}
+
+// ------------------------------------------------------------------------------------------
+// Fragment preparation: Q (bf16) and W (fp32 → bf16 hi + lo) into the per-lane register layout
+// of mma.m16n8k16 with the d-permutation of DESIGN.md §"Kernel":
+//   k-step ks = 2j + e, lane (g, q): A regs {a0a1, a2a3, a4a5, a6a7} hold
+//   (row g, d0, d0+1), (row g+8, d0, d0+1), (row g, d0+2, d0+3), (row g+8, d0+2, d0+3),
+//   d0 = 32j + 8q + 4e — exactly the 8 consecutive bf16 a lane's LDG.128 of a K/V row brings.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) {
+  return (uint32_t)lo | ((uint32_t)hi << 16);
+}
+
+__global__ void prep_kernel(const __grid_constant__ PrepParams p) {
+  const int KS = p.head_dim / 16;
+  const int NT = p.NH * p.CPR;
+  const int Hq = p.n_kv_heads * p.gqa;
+  const int R = p.n_ops * p.rows_per_op;
+  const int n_lh = p.n_l * p.n_kv_heads;
+  const int64_t nq_items = (int64_t)n_lh * KS * 32;
+  const int64_t nw_items = (int64_t)n_lh * NT * KS * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq_items + nw_items;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool isq = i < nq_items;
+    int64_t r = isq ? i : i - nq_items;
+    const int lane = (int)(r % 32); r /= 32;
+    const int ks = (int)(r % KS); r /= KS;
+    int tt = 0;
+    if (!isq) { tt = (int)(r % NT); r /= NT; }
+    const int lh = (int)r;
+    const int l = lh / p.n_kv_heads, h = lh % p.n_kv_heads;
+    const int g = lane >> 2, q = lane & 3;
+    const int j = ks >> 1, e = ks & 1;
+    const int d0 = 32 * j + 8 * q + 4 * e;
+    uint16_t vals[2][4];  // [row half 0/1 (A rows g / g+8)][d0..d0+3]
+    if (isq) {
+      for (int hr = 0; hr < 2; ++hr) {
+        const int rho = hr * 8 + g;
+        for (int k = 0; k < 4; ++k) {
+          uint16_t b = 0;
+          if (rho < R) {
+            const int o = rho / p.rows_per_op, rem = rho % p.rows_per_op;
+            const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
+            b = p.q[o][(((size_t)l * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k];
+          }
+          vals[hr][k] = b;
+        }
+      }
+    } else {
+      const int hs = tt / p.CPR, c = tt % p.CPR;
+      const int rho = hs * 8 + g;
+      for (int k = 0; k < 4; ++k) {
+        float w = 0.f;
+        if (rho < R) {
+          const int o = rho / p.rows_per_op, rem = rho % p.rows_per_op;
+          const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
+          if (c < p.op_classes[o])
+            w = p.w[o][((((size_t)c * p.n_layers + l) * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k];
+        }
+        const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
+        vals[0][k] = __bfloat16_as_ushort(hi);  // A rows 0-7: W_hi
+        vals[1][k] = __bfloat16_as_ushort(lo);  // A rows 8-15: W_lo
+      }
+    }
+    uint4 out;
+    out.x = pack2(vals[0][0], vals[0][1]);
+    out.y = pack2(vals[1][0], vals[1][1]);
+    out.z = pack2(vals[0][2], vals[0][3]);
+    out.w = pack2(vals[1][2], vals[1][3]);
+    if (isq) p.qfrag[((int64_t)lh * KS + ks) * 32 + lane] = out;
+    else p.wfrag[(((int64_t)lh * NT + tt) * KS + ks) * 32 + lane] = out;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Routing / reduction kernels on precomputed margins (ko_route, ko_reduce_stats, and the staged
+// executor of ko_score_batch's routed mode).
+// ------------------------------------------------------------------------------------------
+__global__ void route_init_kernel(uint32_t* state, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    state[i] = 1u;
+}
+
+// warp-aggregated append of tuple t (if pred) to the worklist
+__device__ __forceinline__ void append(bool pred, int32_t t, int32_t* wl, unsigned long long* len) {
+  const unsigned mask = __ballot_sync(0xffffffffu, pred);
+  if (!mask) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(len, (unsigned long long)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+  if (pred) wl[base + __popc(mask & ((1u << lane) - 1))] = t;
+}
+
+// tuples reaching stage p.stage (alive ∧ op pending) → worklist
+__global__ void route_reach_kernel(const __grid_constant__ RouteParams p) {
+  const int64_t n = p.subset ? p.n_subset : p.n_tuples;
+  const int64_t n_round = (n + 31) & ~31ll;
+  const bool have = p.stage >= 0 && p.stage < p.plan.n_stages;
+  const int o = have ? p.plan.stage[p.stage].op : 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_round;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    bool pred = false;
+    int32_t t = 0;
+    if (i < n && have) {
+      t = p.subset ? p.subset[i] : (int32_t)i;
+      const uint32_t st = p.tuple_state[t];
+      pred = (st & 1u) && op_status(st, o) == 0;
+    }
+    append(pred, t, p.worklist, p.worklist_len);
+  }
+}
+
+// apply stage p.stage's decision (margins precomputed) to every tuple reaching it
+__global__ void route_apply_kernel(const __grid_constant__ RouteParams p) {
+  __shared__ int s_cnt[kCountsPerPlan];
+  for (int i = threadIdx.x; i < kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const ko_stage& st = p.plan.stage[p.stage];
+  const int o = st.op;
+  int* cnt = s_cnt + 5 + 4 * p.stage;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < p.n_tuples;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t state = p.tuple_state[t];
+    if (!(state & 1u) || op_status(state, o) != 0) continue;
+    const size_t idx = ((size_t)o * p.n_variants + st.variant) * p.n_tuples + t;
+    const int d = decide(p.margins[idx], st, p.n_classes[o]);
+    atomicAdd(&cnt[0], 1);
+    if (d == D_ACCEPT || d == D_RESOLVED) {
+      state |= 1u << (1 + 2 * o);
+      if (d == D_RESOLVED) state |= ((uint32_t)p.classes[idx] & 15u) << (16 + 4 * o);
+      atomicAdd(&cnt[1], 1);
+    } else if (d == D_REJECT) {
+      state = (state & ~1u) | (2u << (1 + 2 * o));
+      atomicAdd(&cnt[2], 1);
+    } else {
+      atomicAdd(&cnt[3], 1);
+    }
+    p.tuple_state[t] = state;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&p.counts[5 + 4 * p.stage + i], (unsigned long long)cnt[i]);
+}
+
+// whole plan on precomputed margins: final state, P_o worklist, full count row
+__global__ void route_plan_kernel(const __grid_constant__ RouteParams p) {
+  __shared__ int s_cnt[kCountsPerPlan];
+  for (int i = threadIdx.x; i < kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int64_t n_round = (p.n_tuples + 31) & ~31ll;  // whole warps reach the ballot in append()
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_round;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    bool alive = false;
+    if (t < p.n_tuples) {
+      float ms[kMaxOps * kMaxVar];
+      int32_t cs[kMaxOps * kMaxVar];
+      for (int s = 0; s < p.plan.n_stages; ++s) {
+        const int idx = p.plan.stage[s].op * p.n_variants + p.plan.stage[s].variant;
+        const size_t gi = (size_t)idx * p.n_tuples + t;
+        ms[idx] = p.margins[gi];
+        cs[idx] = p.classes ? p.classes[gi] : 0;
+      }
+      const uint32_t st = eval_plan(p.plan, ms, cs, p.n_variants, p.n_classes, p.gold, p.n_tuples,
+                                    t, s_cnt);
+      if (p.tuple_state) p.tuple_state[t] = st;
+      alive = st & 1u;
+    }
+    if (p.worklist) append(alive, (int32_t)t, p.worklist, p.worklist_len);
+  }
+  flush_counts(s_cnt, 1, p.counts);
+}
+
+// TP/FP/FN/|P_o|/|P_g| from the final tuple states of a routed execution
+__global__ void final_counts_kernel(const __grid_constant__ RouteParams p) {
+  __shared__ int s_cnt[kCountsPerPlan];
+  for (int i = threadIdx.x; i < kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  uint32_t referenced = 0;
+  for (int s = 0; s < p.plan.n_stages; ++s) referenced |= 1u << p.plan.stage[s].op;
+  const int64_t n = p.subset ? p.n_subset : p.n_tuples;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = p.subset ? p.subset[i] : i;
+    const uint32_t st = p.tuple_state[t];
+    const bool in_out = st & 1u;
+    bool in_gold = p.gold != nullptr, maps_ok = true;
+    if (p.gold) {
+      for (int o = 0; o < kMaxOps; ++o) {
+        if (!(referenced & (1u << o))) continue;
+        const uint8_t gv = p.gold[(int64_t)o * p.n_tuples + t];
+        if (p.n_classes[o] <= 1) {
+          if (gv != 1) in_gold = false;
+        } else if (((st >> (16 + 4 * o)) & 15u) != gv || op_status(st, o) != 1) {
+          maps_ok = false;
+        }
+      }
+    }
+    if (in_out) atomicAdd(&s_cnt[KO_C_OUT], 1);
+    if (in_gold) atomicAdd(&s_cnt[KO_C_GOLD], 1);
+    if (in_out && in_gold && maps_ok) atomicAdd(&s_cnt[KO_C_TP], 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 5; k += blockDim.x) {
+    long long v = s_cnt[k];
+    if (k == KO_C_FP) v = (long long)s_cnt[KO_C_OUT] - s_cnt[KO_C_TP];
+    if (k == KO_C_FN) v = (long long)s_cnt[KO_C_GOLD] - s_cnt[KO_C_TP];
+    if (v) atomicAdd(&p.counts[k], (unsigned long long)v);
+  }
+}
+
+// G-plan grid on precomputed margins: one warp per tuple, one lane per plan
+__global__ void reduce_kernel(const __grid_constant__ ReduceParams p) {
+  __shared__ int s_cnt[kMaxPlans * kCountsPerPlan];
+  __shared__ float s_m[8][kMaxOps * kMaxVar];
+  __shared__ int32_t s_c[8][kMaxOps * kMaxVar];
+  for (int i = threadIdx.x; i < p.n_plans * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const int nmv = p.n_ops * p.n_variants;
+  for (int64_t t = (int64_t)blockIdx.x * nw + w; t < p.n_tuples; t += (int64_t)gridDim.x * nw) {
+    for (int idx = lane; idx < nmv; idx += 32) {
+      s_m[w][idx] = p.margins[(size_t)idx * p.n_tuples + t];
+      s_c[w][idx] = p.classes ? p.classes[(size_t)idx * p.n_tuples + t] : 0;
+    }
+    __syncwarp();
+    for (int gp = lane; gp < p.n_plans; gp += 32)
+      eval_plan(p.plans[gp], s_m[w], s_c[w], p.n_variants, p.n_classes, p.gold, p.n_tuples, t,
+                s_cnt + gp * kCountsPerPlan);
+    __syncwarp();
+  }
+  flush_counts(s_cnt, p.n_plans, p.counts);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int D, int NH, int CPR>
+cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t s) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ko_score_kernel<D, NH, CPR>, kThreads, 0);
+    if (occ < 1) occ = 1;
+  }
+  const int64_t warps_needed = max_units > 0 ? max_units : 1;
+  int64_t grid = (int64_t)num_sms() * occ;
+  const int64_t need = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  ko_score_kernel<D, NH, CPR><<<(unsigned)grid, kThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_prep(const PrepParams& p, cudaStream_t s) {
+  prep_kernel<<<num_sms() * 2, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_score(const ScoreParams& p, int head_dim, int NH, int CPR, int64_t max_units,
+                         cudaStream_t s) {
+#define KO_DISPATCH(DD, HH, CC) \
+  if (head_dim == DD && NH == HH && CPR == CC) return launch_score_t<DD, HH, CC>(p, max_units, s);
+#define KO_DISPATCH_D(DD)                                                          \
+  KO_DISPATCH(DD, 1, 1) KO_DISPATCH(DD, 1, 2) KO_DISPATCH(DD, 1, 4) KO_DISPATCH(DD, 1, 8) \
+  KO_DISPATCH(DD, 2, 1) KO_DISPATCH(DD, 2, 2) KO_DISPATCH(DD, 2, 4) KO_DISPATCH(DD, 2, 8)
+  KO_DISPATCH_D(64)
+  KO_DISPATCH_D(128)
+#undef KO_DISPATCH_D
+#undef KO_DISPATCH
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_route_init(uint32_t* state, int64_t n, cudaStream_t s) {
+  route_init_kernel<<<num_sms() * 4, 256, 0, s>>>(state, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_route_reach(const RouteParams& p, cudaStream_t s) {
+  route_reach_kernel<<<num_sms() * 4, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_route_apply(const RouteParams& p, cudaStream_t s) {
+  route_apply_kernel<<<num_sms() * 4, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_route_plan(const RouteParams& p, cudaStream_t s) {
+  route_plan_kernel<<<num_sms() * 4, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_final_counts(const RouteParams& p, cudaStream_t s) {
+  final_counts_kernel<<<num_sms() * 2, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_reduce(const ReduceParams& p, cudaStream_t s) {
+  reduce_kernel<<<num_sms() * 2, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ko

@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+Tolerances: margins 2e-3 absolute; decisions and counts bit-exact outside the 1e-2 ambiguity band
+(tests/parity.py)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import kogen  # noqa: E402
+import oracle  # noqa: E402
+from kogen import workloads  # noqa: E402
+from kogen.device import device_workload, tensors_to_device  # noqa: E402
+from tests import parity  # noqa: E402
+from tests.helpers import Geom, build_pool, random_problem  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ko():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2602_04430_b200 as ko
+    return ko
+
+
+def run_oracle_on_host(pool, indptr, ids, sl, geom, ops, variants):
+    return oracle.score(geom, pool, indptr, ids, sl, ops, variants)
+
+
+CASES = [
+    # (name, geom, lengths, classes, variants)
+    ("d64_g1", Geom(1, 1, 1, 64, 1), [128] * 5 + [1, 7, 16, 17, 100], (1,),
+     [(1000, 1), (500, 1), (137, 1)]),
+    ("d128_g4_2ops", Geom(2, 2, 4, 128, 1), [1, 15, 16, 33, 64, 200, 257], (1, 1),
+     [(1000, 2), (500, 2), (200, 1), (1, 1)]),
+    ("d128_map4", Geom(2, 2, 4, 128, 1), [5, 31, 48, 130], (4,), [(1000, 2), (300, 1)]),
+    ("d64_rows12_maps", Geom(2, 1, 4, 64, 1), [3, 40, 77], (1, 3, 1), [(1000, 2), (600, 2), (250, 1)]),
+    ("d128_nq2_rows16", Geom(1, 2, 4, 128, 2), [9, 63, 64, 65], (1, 2), [(1000, 1), (777, 1)]),
+    ("d64_c8", Geom(1, 1, 2, 64, 1), [20, 50], (8,), [(1000, 1)]),
+]
+
+
+@pytest.mark.parametrize("name,geom,lengths,classes,variants", CASES, ids=[c[0] for c in CASES])
+def test_score_parity_random(ko, name, geom, lengths, classes, variants):
+    rng = np.random.default_rng(abs(hash(name)) % 2**32)
+    K, V, ops_h = random_problem(rng, geom, lengths, n_ops=len(classes), classes=classes)
+    pool, indptr, ids, sl = build_pool(K, V, lengths, poison=True)
+    m_or, c_or = run_oracle_on_host(pool, indptr, ids, sl, geom, ops_h, variants)
+    kv, ops = tensors_to_device(pool, indptr, ids, sl, geom, ops_h)
+    m, c, _ = ko.score_batch(kv, ops, variants)
+    torch.cuda.synchronize()
+    err = parity.assert_margins(m.cpu().numpy(), m_or)
+    parity.assert_classes(c.cpu().numpy(), c_or, m_or, classes)
+    assert err < 1e-3
+
+
+def test_c1_grid_parity_and_counts(ko):
+    wl = workloads.get("C1")
+    d = device_workload(wl)
+    m, c, counts = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=wl.plans, gold=d["gold"])
+    torch.cuda.synchronize()
+    m_or, c_or = oracle.score_workload(wl, np.arange(wl.n_tuples))
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    parity.assert_margins(mg, m_or)
+    gold = d["gold"].cpu().numpy()
+    parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, wl.plans, wl.spec.op_classes,
+                         gold)
+
+
+def test_generator_twin_bitwise(ko):
+    """Device fill ≡ host fill (the fixture both sides consume)."""
+    for name, tids in (("C5", [0, 1, 777, 4095]), ("C3", [0, 5, 99])):
+        wl = workloads.get(name)
+        n = max(tids) + 1
+        d = device_workload(wl, n=n, placement="affine")
+        pool_d = d["kv"].pool.view(torch.int16).cpu().numpy().view(np.uint16)
+        for t in tids:
+            hp, hi, hid, hsl = kogen.host_pool(wl.spec, [t], placement="contiguous")
+            L = int(hsl[0])
+            for pi in range(int(hi[1])):
+                dp = pool_d[d["page_ids"][d["indptr"][t] + pi]]
+                hpg = hp[pi]
+                valid = min(16, L - 16 * pi)
+                assert np.array_equal(dp[:, :, :, :valid], hpg[:, :, :, :valid]), (name, t, pi)
+                if valid < 16:                   # device poisons the unused tail slots
+                    assert np.all(dp[:, :, :, valid:] == 0x7FC0)
+
+
+def test_determinism_order_and_placement(ko):
+    wl = workloads.get("C5")
+    n = 300
+    d = device_workload(wl, n=n)
+    m1, _, c1 = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=wl.plans, gold=d["gold"])
+    m2, _, c2 = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=wl.plans, gold=d["gold"])
+    perm = torch.randperm(n, generator=torch.Generator().manual_seed(0)).to(torch.int32).cuda()
+    m3, _, c3 = ko.score_batch(d["kv"], d["ops"], wl.variants, tuple_idx=perm, plans=wl.plans,
+                               gold=d["gold"])
+    d2 = device_workload(wl, n=n, placement="contiguous")
+    m4, _, _ = ko.score_batch(d2["kv"], d2["ops"], wl.variants)
+    torch.cuda.synchronize()
+    assert torch.equal(m1, m2) and torch.equal(c1, c2)
+    assert torch.equal(m1, m3) and torch.equal(c1, c3)
+    assert torch.equal(m1, m4)
+
+
+def test_sharded_counts_add_up(ko):
+    """Σ of k shard passes (tuple subsets) = 1-shard counts, bit-exact (multi-GPU contract)."""
+    wl = workloads.get("C5")
+    n = 500
+    d = device_workload(wl, n=n)
+    _, _, full = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=wl.plans, gold=d["gold"])
+    acc = torch.zeros_like(full)
+    idx = torch.arange(n, dtype=torch.int32, device="cuda")
+    for shard in torch.tensor_split(idx, 3):
+        ko.score_batch(d["kv"], d["ops"], wl.variants, tuple_idx=shard.contiguous(),
+                       plans=wl.plans, gold=d["gold"], counts=acc)
+    torch.cuda.synchronize()
+    assert torch.equal(full, acc)
+
+
+def test_reduce_and_route_exact_on_given_margins(ko):
+    """ko_reduce_stats / ko_route on fixed margins equal the oracle's plan evaluation exactly."""
+    rng = np.random.default_rng(0)
+    n = 3000
+    m = rng.normal(0, 2, size=(3, 2, n)).astype(np.float32)
+    cls = rng.integers(0, 4, size=(3, 2, n)).astype(np.int32)
+    n_classes = [1, 4, 1]
+    gold = np.stack([rng.random(n) < 0.5, rng.integers(0, 4, n), rng.random(n) < 0.4]).astype(np.uint8)
+    plans = [[(0, 0, -1.0, 1.0, 0), (0, 1, 0.0, 0.0, 1), (1, 0, 1.5, 1.5, 0), (1, 1, 0.0, 0.0, 1),
+              (2, 0, -0.5, 0.5, 0), (2, 1, 0.25, 0.25, 1)],
+             [(2, 1, 0.0, 0.0, 1), (0, 0, -2.0, 0.5, 0), (0, 1, 0.0, 0.0, 1)],
+             [(1, 1, 0.0, 0.0, 1)]]
+    mt, ct, gt = (torch.from_numpy(x).cuda() for x in (m, cls, gold))
+    counts = ko.reduce_stats(plans, mt, ct, n_classes, gold=gt)
+    expect = oracle.run_plans(plans, m.astype(np.float64), cls, n_classes, gold)
+    assert np.array_equal(counts.cpu().numpy(), expect)
+    # whole plan via ko_route(stage = -1) and stage by stage via ko_route(stage = s)
+    for pl, ex in zip(plans, expect):
+        st = torch.ones(n, dtype=torch.int32, device="cuda")
+        wl_ = torch.empty(n, dtype=torch.int32, device="cuda")
+        wlen = torch.zeros(1, dtype=torch.int64, device="cuda")
+        c = ko.route(pl, mt, ct, n_classes, -1, st, wl_, wlen, gold=gt)
+        assert np.array_equal(c.cpu().numpy()[0], ex)
+        assert int(wlen.item()) == ex[3]
+        st2 = torch.ones(n, dtype=torch.int32, device="cuda")
+        c2 = torch.zeros((1, 37), dtype=torch.int64, device="cuda")
+        for s in range(len(pl)):
+            ko.route(pl, mt, ct, n_classes, s, st2, wl_, wlen, counts=c2)
+            if s + 1 < len(pl):   # the worklist is exactly the set reaching stage s+1
+                got = set(wl_[:int(wlen.item())].cpu().tolist())
+                o_next = pl[s + 1][0]
+                sv = st2.cpu().numpy().astype(np.uint32)
+                want = set(np.nonzero((sv & 1) & (((sv >> (1 + 2 * o_next)) & 3) == 0))[0].tolist())
+                assert got == want
+        assert torch.equal(st, st2)
+        assert np.array_equal(c2.cpu().numpy()[0, 5:], ex[5:])
+
+
+def test_routed_mode_parity(ko):
+    """Routed execution (n_plans == 1) of a filter → map → filter cascade plan."""
+    wl = workloads.get("C4")
+    n = 2000
+    d = device_workload(wl, n=n)
+    plan = wl.plans[0]
+    m, c, counts = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan], gold=d["gold"])
+    torch.cuda.synchronize()
+    m_or, c_or = oracle.score_workload(wl, np.arange(n))
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    reached = np.isfinite(mg)
+    parity.assert_margins(mg, m_or, mask=reached)
+    gold = d["gold"].cpu().numpy()
+    parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], wl.spec.op_classes, gold)
+    # grid mode on the same plan gives the same counts (execution strategy does not matter)
+    mg2, cg2, cnt2 = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan, plan], gold=d["gold"])
+    torch.cuda.synchronize()
+    assert np.array_equal(cnt2.cpu().numpy()[0], counts.cpu().numpy()[0])
+
+
+def test_empty_and_single_token(ko):
+    geom = Geom(1, 1, 1, 64, 1)
+    rng = np.random.default_rng(1)
+    K, V, ops_h = random_problem(rng, geom, [1, 1, 2])
+    pool, indptr, ids, sl = build_pool(K, V, [1, 1, 2], poison=True)
+    kv, ops = tensors_to_device(pool, indptr, ids, sl, geom, ops_h)
+    m_or, _ = oracle.score(geom, pool, indptr, ids, sl, ops_h, [(1000, 1), (1, 1)])
+    m, _, _ = ko.score_batch(kv, ops, [(1000, 1), (1, 1)])
+    torch.cuda.synchronize()
+    parity.assert_margins(m.cpu().numpy(), m_or, tol=1e-4)
+    empty = torch.empty(0, dtype=torch.int32, device="cuda")
+    m2 = torch.full_like(m, 7.0)
+    ko.score_batch(kv, ops, [(1000, 1), (1, 1)], tuple_idx=empty, margins=m2)
+    torch.cuda.synchronize()
+    assert torch.all(m2 == 7.0)
+
+
+def test_error_paths(ko):
+    wl = workloads.get("C1")
+    d = device_workload(wl, n=4)
+    with pytest.raises(ko.KoError, match="keep_permille"):
+        ko.score_batch(d["kv"], d["ops"], [(0, 1)])
+    with pytest.raises(ko.KoError, match="layer_cut"):
+        ko.score_batch(d["kv"], d["ops"], [(1000, 2)])
+    with pytest.raises(ko.KoError, match="no final"):
+        ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[[(0, 1, -1, 1, 0)], [(0, 0, 0, 0, 1)]])
+    ws = torch.empty(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ko.KoError, match="workspace"):
+        ko.score_batch(d["kv"], d["ops"], wl.variants, workspace=ws)
