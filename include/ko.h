@@ -125,7 +125,7 @@ typedef struct {
  *
  * kv, ops[n_ops], variants[n_variants]: as above.
  * tuple_idx: device int32 [n_idx] tuple ids to process (any order, no duplicates), or NULL = all
- *            n_tuples.
+ *            n_tuples (n_idx ignored).  n_idx == 0 with a non-NULL tuple_idx is a no-op.
  * margins:   device fp32 [n_ops][n_variants][n_tuples], indexed by tuple id (may be NULL only in
  *            routed mode).  classes: device int32, same shape, argmax class (0 for filters); may
  *            be NULL.

@@ -214,6 +214,8 @@ def score_batch(kv: KVCache, ops: Sequence[Operator], variants: Sequence[Tuple[i
     if counts is None and n_plans:
         counts = torch.zeros((n_plans, COUNTS_PER_PLAN), dtype=torch.int64, device=dev)
     n_work = n if tuple_idx is None else int(tuple_idx.numel())
+    if tuple_idx is not None and n_work == 0:
+        return margins, classes, counts      # empty selection: nothing to score or count
     if workspace is None:
         workspace = alloc_workspace(kv, ops, n_var, n_work)
     parr = make_plans(plans) if n_plans else None

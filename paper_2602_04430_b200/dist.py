@@ -1,0 +1,40 @@
+"""Multi-GPU plumbing of the pass: tuples shard across ranks, each rank scores its
+own shard from its own pool, and the only exchange is one all-reduce(SUM) of the int64 count
+vector.  Integer sums make N-rank counts bit-identical to one rank.  torch.distributed supplies
+the process group (NCCL on B200; gloo in the CPU tests)."""
+from __future__ import annotations
+
+from typing import Tuple
+
+
+def shard_range(n_total: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous tuple range [begin, end) of `rank` (sizes differ by at most one)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(n_total, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def weak_shard(n_per_rank: int, rank: int) -> Tuple[int, int]:
+    """Weak scaling: rank r owns tuple ids r·n .. r·n + n − 1 of an N·n-tuple dataset."""
+    return rank * n_per_rank, (rank + 1) * n_per_rank
+
+
+def combine_counts(counts, group=None):
+    """In-place all-reduce(SUM) of an int64 count tensor across the process group."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    return counts
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    """Max of a per-rank scalar (device time) over the group — the timing rule of bench.py."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

@@ -1,0 +1,75 @@
+"""N > 1 path on CPU (gloo, world size 2): tuple sharding + the count all-reduce give exactly the
+1-rank counts, and the timing combine is a max over ranks.  The per-rank counts come from the
+oracle's plan evaluation on that rank's shard (the GPU path's counts obey the same contract,
+checked on the GPU by test_sharded_counts_add_up)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2602_04430_b200 import dist as kodist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _problem(n=1001):
+    rng = np.random.default_rng(42)
+    m = rng.normal(0, 2, size=(2, 3, n))
+    gold = (rng.random((2, n)) < 0.45).astype(np.uint8)
+    plans = [[(0, 0, -1.0, 1.0, 0), (0, 2, 0.0, 0.0, 1), (1, 1, -0.5, 0.5, 0), (1, 2, 0.0, 0.0, 1)],
+             [(1, 2, 0.0, 0.0, 1), (0, 0, 0.0, 0.0, 1)]]
+    return m, gold, plans
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, gold, plans = _problem()
+    b, e = kodist.shard_range(m.shape[2], rank, world)
+    c = oracle.run_plans(plans, m[:, :, b:e], np.zeros((2, 3, e - b), np.int32), [1, 1],
+                         gold[:, b:e])
+    t = torch.from_numpy(c)
+    kodist.combine_counts(t)
+    tmax = kodist.max_over_ranks(float(rank + 1))
+    if rank == 0:
+        out.put((t.numpy().tolist(), tmax))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_counts_equal_single_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    counts, tmax = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m, gold, plans = _problem()
+    full = oracle.run_plans(plans, m, np.zeros(m.shape, np.int32), [1, 1], gold)
+    assert np.array_equal(np.array(counts), full)
+    assert tmax == 2.0
+
+
+@pytest.mark.parametrize("n,world", [(10, 3), (7, 7), (0, 2), (1000, 8)])
+def test_shard_range_partitions(n, world):
+    seen = []
+    for r in range(world):
+        b, e = kodist.shard_range(n, r, world)
+        seen += list(range(b, e))
+        assert e - b in (n // world, n // world + 1)
+    assert seen == list(range(n))
