@@ -54,6 +54,28 @@ def n_kept(L, keep):
     return np.maximum(1, (L.astype(np.int64) * keep) // 1000)
 
 
+def algorithmic_bytes_routed(wl, seq_len, margins):
+    """Routed mode: need(t,l) = largest n_kept over the (op, variant) entries the GPU itself
+    reached for tuple t (finite margins, §8(d)) whose layer cut includes l."""
+    sp = wl.spec
+    reached = np.isfinite(margins)                     # [n_ops][n_var][n]
+    need_tokens = 0
+    for l in range(sp.n_layers):
+        need = np.zeros(len(seq_len), np.int64)
+        for v, (k, c) in enumerate(wl.variants):
+            if c <= l:
+                continue
+            hit = reached[:, v, :].any(axis=0)
+            need = np.maximum(need, np.where(hit, n_kept(seq_len, k), 0))
+        need_tokens += int(need.sum())
+    kv = need_tokens * sp.n_kv_heads * 4 * sp.head_dim
+    n = len(seq_len)
+    pages = int(((seq_len.astype(np.int64) + 15) // 16).sum())
+    meta = 4 * pages + 12 * n
+    out = 8 * int(reached.sum())
+    return kv + meta + sp.n_ops * n + out, kv
+
+
 def algorithmic_bytes(wl, seq_len, n_plans):
     """Σ_t Σ_l Hkv·4·d·need(t,l) (need = largest prefix any variant with cut > l
     consults; nested prefixes count once) + 4 B per page-table entry + 4 B seq_len + 8 B indptr
@@ -215,8 +237,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     wl = workloads.get(args.config)
-    n = args.n_tuples or wl.n_tuples
-    t0 = rank * n
+    n = args.n_tuples or wl.bench_n or wl.n_tuples
+    t0 = rank * n                   # weak scaling: rank r owns tuple ids r·n .. r·n + n − 1
     d = device_workload(wl, t0=t0, n=n, placement="contiguous")
     kv, ops, gold = d["kv"], d["ops"], d["gold"]
     n_var, n_ops = len(wl.variants), wl.spec.n_ops
@@ -265,9 +287,12 @@ def main():
     ms_step = ms_total / args.steps
     value = world * n * args.steps / (ms_total / 1000.0)
 
-    # parity spot-check of the timed outputs: counts == oracle plan evaluation of the GPU margins
     cnt = counts.cpu().numpy()
-    alg_bytes, kv_bytes = algorithmic_bytes(wl, d["seq_len"], len(plans))
+    routed = len(plans) == 1
+    if routed:
+        alg_bytes, kv_bytes = algorithmic_bytes_routed(wl, d["seq_len"], margins.cpu().numpy())
+    else:
+        alg_bytes, kv_bytes = algorithmic_bytes(wl, d["seq_len"], len(plans))
     peak, peak_src = measured_peak()
     achieved = alg_bytes / (kern_ms / 1000.0) / 1e9
     key = f"{wl.name}:{n}"
@@ -289,7 +314,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{wl.name}: {wl.desc}", "n_tuples_per_rank": n,
-                       "mode": "grid (all ops x variants in one read + per-tuple plan grid)",
+                       "mode": ("routed (plan stages in order, only reached tuples scored)"
+                                if routed else
+                                "grid (all ops x variants in one read + per-tuple plan grid)"),
                        "n_plans": len(plans), "variants": wl.variants,
                        "kv_bytes_per_rank": kv_bytes,
                        "l2": "inputs larger than L2 (KV per rank >> 126 MB); no flush",
@@ -300,7 +327,7 @@ def main():
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "cpu_baseline": cb,
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": (3 * len(plans[0]) + 2 if routed else 2) * args.steps,
             "clocks": clk.summary(),
             "counts_plan0": cnt[0, :5].tolist(),
         }

@@ -31,6 +31,7 @@ class Workload:
     plans: List[List[Stage]]
     mode: str = "grid"                         # "grid" (profiling + plan grid) or "routed"
     bias: Optional[List[List[float]]] = None   # [op][class]
+    bench_n: int = 0                           # tuples per rank per bench step (resident batch)
 
     def biases(self) -> List[List[float]]:
         if self.bias is not None:
@@ -62,7 +63,7 @@ def c1() -> Workload:
     variants = [(1000, 1), (500, 1)]
     plans = [[_sym(0, 1, h), _final(0, 0)] for h in (0.5, 1.0, 2.0)]
     return Workload("C1", "single semantic filter, 64 tuples, 1 KV head, head_dim 64, 1 layer, "
-                    "prefix 128, 3 threshold variants", spec, 64, variants, 0, plans)
+                    "prefix 128, 3 threshold variants", spec, 64, variants, 0, plans, bench_n=64)
 
 
 def c2() -> Workload:
@@ -76,7 +77,7 @@ def c2() -> Workload:
                           _sym(1, 0, h2), _sym(1, 1, h2), _final(1, 2)])
     return Workload("C2", "two-filter conjunctive pipeline, 10k tuples, 8 KV heads GQA 4:1, "
                     "head_dim 128, 4 layers, prefix 512, global recall target 0.9",
-                    spec, 10_000, variants, 2, plans)
+                    spec, 10_000, variants, 2, plans, bench_n=10_000)
 
 
 def c3() -> Workload:
@@ -85,7 +86,8 @@ def c3() -> Workload:
     variants = [(k, c) for c in (1, 2) for k in (1000, 500, 200)]
     plans = [[_final(0, v)] for v in range(len(variants))]
     return Workload("C3", "100k documents, variable prefix 256-4096 in 16-token pages, sweep of "
-                    "prefix/layer-cut variants", spec, 100_000, variants, 3, plans)
+                    "prefix/layer-cut variants", spec, 100_000, variants, 3, plans,
+                    bench_n=10_000)     # 1.13 TB total: resident batches of 10 k docs (~113 GB)
 
 
 def c4() -> Workload:
@@ -95,7 +97,8 @@ def c4() -> Workload:
     plans = [[_sym(0, 0, 1.0), _final(0, 1), (1, 0, 2.0, 2.0, 0), _final(1, 1),
               _sym(2, 0, 1.0), _final(2, 1)]]
     return Workload("C4", "three-operator pipeline filter->map-classify->filter, small->large "
-                    "cascades, 1M tuples", spec, 1_000_000, variants, 1, plans, mode="routed")
+                    "cascades, 1M tuples", spec, 1_000_000, variants, 1, plans, mode="routed",
+                    bench_n=125_000)    # 1M sharded over 8 GPUs = 125 k per GPU (~131 GB)
 
 
 def c5() -> Workload:
@@ -108,7 +111,8 @@ def c5() -> Workload:
         for v2, h2 in per_op:
             plans.append([_sym(0, v1, h1), _final(0, 0), _sym(1, v2, h2), _final(1, 0)])
     return Workload("C5", "per-pipeline recall/cost statistics over a 50k labelled sample for a "
-                    "64-point threshold/variant grid", spec, 50_000, variants, 0, plans)
+                    "64-point threshold/variant grid", spec, 50_000, variants, 0, plans,
+                    bench_n=50_000)
 
 
 ALL = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}

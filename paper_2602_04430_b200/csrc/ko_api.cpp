@@ -1,6 +1,8 @@
 // ko_api.cpp — the C ABI of libko.so (include/ko.h): host validation, workspace layout, and the
 // orchestration of the sm_100a kernels in ko_kernels.cu.  No allocation happens in a call; every
 // launch goes on the caller's stream.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -158,6 +160,37 @@ int max_classes(const ko_operator* ops, int n_ops) {
   return m;
 }
 
+// TMA descriptor of the pool: 5-D bf16 view, innermost first: (head_dim, 16 tokens, kv-head,
+// 2·layer + {K,V}, page); box (64, 16, 1, 2, 1) = the K and V rows of one kv-head of one layer of
+// one page for 64 head dims; SWIZZLE_128B (conflict-free fragment reads, see ko_kernels.cu).
+ko_status make_tmap(CUtensorMap* map, const ko_kv_cache* kv) {
+  const cuuint64_t D = (cuuint64_t)kv->head_dim;
+  cuuint64_t dims[5] = {D, 16, (cuuint64_t)kv->n_kv_heads, (cuuint64_t)(2 * kv->n_layers),
+                        (cuuint64_t)std::max<int64_t>(kv->n_pages, 1)};
+  cuuint64_t strides[4] = {D * 2, 16 * D * 2, (cuuint64_t)kv->n_kv_heads * 16 * D * 2,
+                           (cuuint64_t)(2 * kv->n_layers) * kv->n_kv_heads * 16 * D * 2};
+  cuuint32_t box[5] = {64, 16, 1, 2, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  // the driver entry point is resolved through the runtime, so libko.so does not link libcuda
+  // (the host-only parts of the ABI load on machines without a driver)
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+      return fail(KO_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                                      const_cast<void*>(kv->kv_pool), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KO_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return KO_OK;
+}
+
 // fill the kv/op/variant part of ScoreParams and the matching PrepParams for a set of local ops
 void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
                  const ko_operator* ops, const int* op_sel, int n_sel, const ko_variant* variants,
@@ -283,6 +316,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     ko::PrepParams pp;
     fill_common(sp, pp, kv, ops, op_sel, n_ops, variants, var_sel, n_variants, n_ops, n_variants,
                 ws, CPR, NH);
+    if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
     sp.work = tuple_idx;
     sp.work_len_host = n_work;
     sp.work_len_dev = nullptr;
@@ -333,6 +367,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     ko::ScoreParams sp;
     ko::PrepParams pp;
     fill_common(sp, pp, kv, ops, op_sel, 1, variants, var_sel, 1, n_ops, n_variants, ws, CPR, NH);
+    if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
     sp.work = ws.worklist;
     sp.work_len_host = 0;
     sp.work_len_dev = (const int64_t*)ws.worklist_len;

@@ -2,6 +2,7 @@
 // ko_kernels.cu (device code + launchers).  Not part of the public ABI (that is include/ko.h).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -22,6 +23,9 @@ enum Mode : int32_t { MODE_GRID = 0, MODE_STAGE = 1 };
 // One launch of the scoring kernel.  "Local" op/variant indices are positions in this launch;
 // op_ids / var_ids map them to the caller's indices (margins layout, plans, gold).
 struct ScoreParams {
+  // TMA descriptor of the pool viewed as 5-D bf16 [n_pages][2·n_layers][n_kv_heads][16][head_dim]
+  // (innermost last), box 64 × 16 × 1 × 2 × 1, 128-byte swizzle
+  alignas(64) CUtensorMap tmap;
   // paged KV store
   const uint16_t* pool;
   int64_t page_elems;  // bf16 elements per page = n_layers*2*n_kv_heads*16*head_dim

@@ -48,14 +48,6 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t a0, const
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint4 ldg_stream(const uint16_t* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
 __device__ __forceinline__ int n_kept(int L, int keep) {  // Q3: max(1, floor(L·keep/1000))
   int n = (int)(((long long)L * keep) / 1000);
   return n < 1 ? 1 : n;
@@ -141,35 +133,98 @@ __device__ void flush_counts(int* s_cnt, int n_rows, unsigned long long* counts)
 // ------------------------------------------------------------------------------------------
 // The scoring kernel
 // ------------------------------------------------------------------------------------------
-template <int KP>
-struct PageRegs {
-  uint4 k[2][KP];
-  uint4 v[2][KP];
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// TMA: one (64 d × 16 tokens × 1 head × {K,V}) box of page `page` → smem (128B-swizzled),
+// completion counted on `bar`; L2 evict-first (the KV stream is read once).
+__device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, int d0, int h,
+                                             int kv0, int page, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(d0), "r"(0), "r"(h), "r"(kv0), "r"(page),
+      "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(addr));
+  return r;
+}
+
+template <int D>
+struct Ring {
+  static constexpr int kBoxBytes = 64 * 16 * 2 * 2;      // 64 d × 16 tokens × {K,V} × bf16
+  static constexpr int kStageBytes = (D / 64) * kBoxBytes;
+  static constexpr int kStages = D == 128 ? 3 : 6;       // per warp
+  static constexpr int kWarpBytes = kStages * kStageBytes;
+  static constexpr int kSmemBytes = (kThreads / 32) * kWarpBytes + 1024;  // + alignment slack
 };
 
 template <int D, int NH, int CPR>
 __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_constant__ ScoreParams p) {
   constexpr int KS = D / 16;  // mma k-steps over head_dim
-  constexpr int KP = D / 32;  // 128-bit loads per token row per lane (each feeds 2 k-steps)
+  constexpr int KP = D / 32;  // 128-bit fragment reads per token row per lane (2 k-steps each)
   constexpr int NT = NH * CPR;
+  constexpr int S = Ring<D>::kStages;
+  constexpr int STAGE = Ring<D>::kStageBytes;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
 
+  extern __shared__ uint8_t smem_dyn[];
   __shared__ int s_cnt[kMaxPlans * kCountsPerPlan];
   __shared__ float s_z[kThreads / 32][kMaxOps * kMaxVar * kMaxCls];
   __shared__ float s_m[kThreads / 32][kMaxOps * kMaxVar];
   __shared__ int32_t s_c[kThreads / 32][kMaxOps * kMaxVar];
+  __shared__ __align__(8) uint64_t s_full[kThreads / 32][S];
+
+  // per-warp ring of S stages (1024-byte aligned for the 128B swizzle atom)
+  uint8_t* ring_base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* ring = ring_base + warp * Ring<D>::kWarpBytes;
+  const uint32_t ring_s = smem_u32(ring);
 
   const int n_cnt_rows = p.mode == MODE_GRID ? p.n_plans : (p.tuple_state ? 1 : 0);
   for (int i = threadIdx.x; i < n_cnt_rows * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&s_full[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap)) : "memory");
   __syncthreads();
+  uint64_t policy = 0;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
 
   const int64_t n_work = p.work_len_dev ? *p.work_len_dev : p.work_len_host;
   const int Hkv = p.n_kv_heads;
   const int upt = p.n_l * Hkv;  // units per tuple
   const int64_t n_units = n_work * upt;
   const int R = p.n_ops * p.rows_per_op;
-  const int64_t kv_stride = (int64_t)Hkv * 16 * D;  // K block → V block
 
   // row slot → local op for this lane's two half-slots
   int slot_op[NH];
@@ -178,6 +233,15 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     const int rho = hs * 8 + g;
     slot_op[hs] = rho < R ? rho / p.rows_per_op : -1;
   }
+
+  // lane-constant smem offsets of this lane's fragment reads inside a stage: token row g (+8),
+  // d-chunk (2q + (j & 1)) of box (j >> 1), XOR-swizzled by the row (= token mod 8)
+  uint32_t frag_off[KP];
+#pragma unroll
+  for (int j = 0; j < KP; ++j)
+    frag_off[j] = (j >> 1) * Ring<D>::kBoxBytes + g * 128 + ((((2 * q) + (j & 1)) ^ g) << 4);
+
+  uint32_t issued = 0, consumed = 0;  // ring positions (warp-uniform, persistent across units)
 
   for (;;) {
     long long u = 0;
@@ -197,6 +261,35 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     int next_snap = n_need;  // smallest active n_kept (first snapshot point)
     for (int v = 0; v < p.n_var; ++v)
       if (p.cut[v] > l) next_snap = min(next_snap, n_kept(L, p.keep[v]));
+
+    const int64_t pbase = p.page_indptr[t];
+    const int n_pages = (n_need + 15) >> 4;
+    int pid_chunk = 0;
+    int pid_reg = lane < n_pages ? __ldg(p.page_ids + pbase + lane) : 0;
+
+    // TMA issue of page `pg` of this unit into the next ring slot (whole warp calls; lane 0 acts)
+    auto issue = [&](int pg) {
+      const int chunk = pg >> 5;
+      if (chunk != pid_chunk) {
+        const int idx = (chunk << 5) + lane;
+        pid_reg = idx < n_pages ? __ldg(p.page_ids + pbase + idx) : 0;
+        pid_chunk = chunk;
+      }
+      const int pid = __shfl_sync(0xffffffffu, pid_reg, pg & 31);
+      if (lane == 0) {
+        const int slot = issued % S;
+        uint64_t* bar = &s_full[warp][slot];
+        mbar_expect_tx(bar, STAGE);
+        uint8_t* dst = ring + slot * STAGE;
+#pragma unroll
+        for (int b = 0; b < D / 64; ++b)
+          tma_load_box(dst + b * Ring<D>::kBoxBytes, &p.tmap, 64 * b, h, 2 * l, pid, bar, policy);
+      }
+      ++issued;
+    };
+    // prologue: fill the ring (all earlier stages have been consumed)
+    const int n_pro = min(S, n_pages);
+    for (int k = 0; k < n_pro; ++k) issue(k);
 
     // operator-query fragments for (l, h)
     const int lh = l * Hkv + h;
@@ -226,57 +319,38 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       for (int c = 0; c < CPR; ++c) ac[hs][c] = 0.f;
     }
 
-    const int64_t pbase = p.page_indptr[t];
-    const int n_pages = (n_need + 15) >> 4;
-    const size_t koff = ((size_t)(l * 2) * Hkv + h) * 16 * D;
-    int pid_chunk = -1;
-    int pid_reg = 0;
-
-    auto page_id = [&](int pg) -> int64_t {
-      const int chunk = pg >> 5;
-      if (chunk != pid_chunk) {
-        const int idx = (chunk << 5) + lane;
-        pid_reg = idx < n_pages ? __ldg(p.page_ids + pbase + idx) : 0;
-        pid_chunk = chunk;
-      }
-      return (int64_t)__shfl_sync(0xffffffffu, pid_reg, pg & 31);
-    };
-
-    auto load_page = [&](PageRegs<KP>& r, int pg) {
-      const uint16_t* kb = p.pool + page_id(pg) * p.page_elems + koff;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int tok = nt * 8 + g;
-        const bool valid = (pg * 16 + tok) < n_need;
-        const uint16_t* kr = kb + tok * D + 8 * q;
-#pragma unroll
-        for (int j = 0; j < KP; ++j) {
-          r.k[nt][j] = valid ? ldg_stream(kr + 32 * j) : make_uint4(0, 0, 0, 0);
-          r.v[nt][j] = valid ? ldg_stream(kr + kv_stride + 32 * j) : make_uint4(0, 0, 0, 0);
-        }
-      }
-    };
-
     int snap_lo = 0;  // first token not yet folded into the running state
 
-    auto process_page = [&](const PageRegs<KP>& r, int pg) {
+    for (int pg = 0; pg < n_pages; ++pg) {
+      const int slot = consumed % S;
+      mbar_wait(&s_full[warp][slot], (consumed / S) & 1u);
+      const uint32_t stage = ring_s + slot * STAGE;
       // ---- tensor cores: S = Q·Kᵀ and U = W·Vᵀ for this page's 16 tokens
-      float S[2][4];
+      float Sacc[2][4];
       float U[NT][2][4];
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
+        const bool valid = (pg * 16 + nt * 8 + g) < n_need;  // B-operand row = token nt*8+g
+        uint4 kf[KP], vf[KP];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) S[nt][i] = 0.f;
+        for (int j = 0; j < KP; ++j) {
+          const uint32_t a = stage + frag_off[j] + nt * 8 * 128;
+          kf[j] = lds128(a);
+          vf[j] = lds128(a + 16 * 128);  // V rows follow the 16 K rows of the box
+          if (!valid) { kf[j] = make_uint4(0, 0, 0, 0); vf[j] = make_uint4(0, 0, 0, 0); }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Sacc[nt][i] = 0.f;
 #pragma unroll
         for (int tt = 0; tt < NT; ++tt)
 #pragma unroll
           for (int i = 0; i < 4; ++i) U[tt][nt][i] = 0.f;
 #pragma unroll
         for (int j = 0; j < KP; ++j) {
-          mma16816(S[nt], qa[2 * j][0], qa[2 * j][1], qa[2 * j][2], qa[2 * j][3], r.k[nt][j].x,
-                   r.k[nt][j].y);
-          mma16816(S[nt], qa[2 * j + 1][0], qa[2 * j + 1][1], qa[2 * j + 1][2], qa[2 * j + 1][3],
-                   r.k[nt][j].z, r.k[nt][j].w);
+          mma16816(Sacc[nt], qa[2 * j][0], qa[2 * j][1], qa[2 * j][2], qa[2 * j][3], kf[j].x,
+                   kf[j].y);
+          mma16816(Sacc[nt], qa[2 * j + 1][0], qa[2 * j + 1][1], qa[2 * j + 1][2],
+                   qa[2 * j + 1][3], kf[j].z, kf[j].w);
         }
 #pragma unroll
         for (int tt = 0; tt < NT; ++tt) {
@@ -292,10 +366,17 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
               a0[0] = f0.x; a0[1] = f0.y; a0[2] = f0.z; a0[3] = f0.w;
               a1[0] = f1.x; a1[1] = f1.y; a1[2] = f1.z; a1[3] = f1.w;
             }
-            mma16816(U[tt][nt], a0[0], a0[1], a0[2], a0[3], r.v[nt][j].x, r.v[nt][j].y);
-            mma16816(U[tt][nt], a1[0], a1[1], a1[2], a1[3], r.v[nt][j].z, r.v[nt][j].w);
+            mma16816(U[tt][nt], a0[0], a0[1], a0[2], a0[3], vf[j].x, vf[j].y);
+            mma16816(U[tt][nt], a1[0], a1[1], a1[2], a1[3], vf[j].z, vf[j].w);
           }
         }
+      }
+      // the stage's bytes are in registers: hand the slot back to TMA for page pg + S
+      __syncwarp();
+      ++consumed;
+      if (pg + S < n_pages) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(pg + S);
       }
       // ---- per-lane token indices and values: k = nt*2 + e ↔ token pg*16 + nt*8 + 2q + e
       const int page_hi = min(pg * 16 + 16, n_need);
@@ -311,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
             const int nt = k >> 1, e = k & 1;
             const int tok = pg * 16 + nt * 8 + 2 * q + e;
             const bool in = tok >= snap_lo && tok < seg_hi;
-            x[k] = in ? S[nt][2 * hs + e] * p.scale_log2 : -CUDART_INF_F;
+            x[k] = in ? Sacc[nt][2 * hs + e] * p.scale_log2 : -CUDART_INF_F;
             xm = fmaxf(xm, x[k]);
           }
           const float mn = fmaxf(mx[hs], xm);
@@ -395,17 +476,6 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         }
         if (snap_lo >= page_hi) break;
       }
-    };
-
-    // ---- page loop, one page of loads in flight ahead of the math
-    PageRegs<KP> ra, rb;
-    load_page(ra, 0);
-    for (int pg = 0; pg < n_pages; pg += 2) {
-      if (pg + 1 < n_pages) load_page(rb, pg + 1);
-      process_page(ra, pg);
-      if (pg + 1 >= n_pages) break;
-      if (pg + 2 < n_pages) load_page(ra, pg + 2);
-      process_page(rb, pg + 1);
     }
 
     // ---- tuple completion: the warp finishing the tuple's last unit finalises it
@@ -492,7 +562,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 // of mma.m16n8k16 with the d-permutation of DESIGN.md §"Kernel":
 //   k-step ks = 2j + e, lane (g, q): A regs {a0a1, a2a3, a4a5, a6a7} hold
 //   (row g, d0, d0+1), (row g+8, d0, d0+1), (row g, d0+2, d0+3), (row g+8, d0+2, d0+3),
-//   d0 = 32j + 8q + 4e — exactly the 8 consecutive bf16 a lane's LDG.128 of a K/V row brings.
+//   d0 = 64(j/2) + 16q + 8(j%2) + 4e — exactly the 8 consecutive bf16 of the 16-byte chunk
+//   (2q + j%2) of 64-wide box j/2 that lane (g, q) reads from the swizzled TMA stage.
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) {
   return (uint32_t)lo | ((uint32_t)hi << 16);
@@ -518,7 +589,7 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
     const int l = lh / p.n_kv_heads, h = lh % p.n_kv_heads;
     const int g = lane >> 2, q = lane & 3;
     const int j = ks >> 1, e = ks & 1;
-    const int d0 = 32 * j + 8 * q + 4 * e;
+    const int d0 = 64 * (j >> 1) + 16 * q + 8 * (j & 1) + 4 * e;  // see frag_off in the kernel
     uint16_t vals[2][4];  // [row half 0/1 (A rows g / g+8)][d0..d0+3]
     if (isq) {
       for (int hr = 0; hr < 2; ++hr) {
@@ -736,8 +807,12 @@ int num_sms() {
 template <int D, int NH, int CPR>
 cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t s) {
   static int occ = 0;
+  constexpr int smem = Ring<D>::kSmemBytes;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ko_score_kernel<D, NH, CPR>, kThreads, 0);
+    cudaFuncSetAttribute(ko_score_kernel<D, NH, CPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ko_score_kernel<D, NH, CPR>, kThreads,
+                                                  smem);
     if (occ < 1) occ = 1;
   }
   const int64_t warps_needed = max_units > 0 ? max_units : 1;
@@ -745,7 +820,7 @@ cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t
   const int64_t need = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  ko_score_kernel<D, NH, CPR><<<(unsigned)grid, kThreads, 0, s>>>(p);
+  ko_score_kernel<D, NH, CPR><<<(unsigned)grid, kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 
