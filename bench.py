@@ -304,6 +304,16 @@ def main():
         e2e = run_e2e(args, ko, torch, wl, d, ops, gold, plans, margins, classes, counts, ws, world,
                       dist)
 
+    # host derivation (row a12 / NEXT-2): cheapest plan of the grid meeting the recall target
+    selection = None
+    if rank == 0 and len(plans) > 1:
+        from paper_2602_04430_b200 import plan_select
+        best, _ = plan_select.select_plan(plans, cnt, wl.variants, target_recall=0.9)
+        selection = {"target_recall": 0.9, "alpha": 0.95,
+                     "plan": None if best is None else best.index,
+                     "cost_vs_gold": None if best is None else best.cost / (world * n * wl.spec.n_ops),
+                     "recall_lb": None if best is None else best.recall_lb}
+
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = oracle_sample(wl, args.cpu_seconds)
@@ -330,6 +340,7 @@ def main():
             "gpu_launches": (3 * len(plans[0]) + 2 if routed else 2) * args.steps,
             "clocks": clk.summary(),
             "counts_plan0": cnt[0, :5].tolist(),
+            "plan_selection": selection,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

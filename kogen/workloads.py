@@ -39,18 +39,24 @@ class Workload:
         cal = load_calibration().get(self.name)
         if cal is None:
             return [[0.0] * c for c in self.spec.op_classes]
-        return cal
+        return cal["bias"]
 
 
 def load_calibration() -> Dict[str, List[List[float]]]:
     if not os.path.exists(CALIBRATION):
         return {}
     with open(CALIBRATION) as f:
-        return json.load(f)
+        return {k: v for k, v in json.load(f).items() if isinstance(v, dict)}
 
 
-def _sym(op: int, var: int, half: float) -> Stage:
-    return (op, var, -half, half, 0)
+def center(name: str, op: int, var: int) -> float:
+    """Calibrated threshold center of (op, variant) (oracle/calibrate.py), 0 if uncalibrated."""
+    cal = load_calibration().get(name)
+    return float(cal["centers"][op][var]) if cal else 0.0
+
+
+def _sym(op: int, var: int, half: float, c: float = 0.0) -> Stage:
+    return (op, var, c - half, c + half, 0)
 
 
 def _final(op: int, var: int, theta: float = 0.0) -> Stage:
@@ -61,7 +67,7 @@ def c1() -> Workload:
     spec = GenSpec(seed=1, n_layers=1, n_kv_heads=1, gqa=1, head_dim=64, n_q=1,
                    op_classes=[1], op_pi_permille=[300], len_min=128, len_max=128, w_log2_den=6)
     variants = [(1000, 1), (500, 1)]
-    plans = [[_sym(0, 1, h), _final(0, 0)] for h in (0.5, 1.0, 2.0)]
+    plans = [[_sym(0, 1, h, center("C1", 0, 1)), _final(0, 0)] for h in (0.5, 1.0, 2.0)]
     return Workload("C1", "single semantic filter, 64 tuples, 1 KV head, head_dim 64, 1 layer, "
                     "prefix 128, 3 threshold variants", spec, 64, variants, 0, plans, bench_n=64)
 
@@ -73,8 +79,10 @@ def c2() -> Workload:
     plans = []
     for h1 in (0.5, 1.0, 2.0, 4.0):          # 4 x 4 grid of per-op half-widths (budget split)
         for h2 in (0.5, 1.0, 2.0, 4.0):
-            plans.append([_sym(0, 0, h1), _sym(0, 1, h1), _final(0, 2),
-                          _sym(1, 0, h2), _sym(1, 1, h2), _final(1, 2)])
+            plans.append([_sym(0, 0, h1, center("C2", 0, 0)), _sym(0, 1, h1, center("C2", 0, 1)),
+                          _final(0, 2),
+                          _sym(1, 0, h2, center("C2", 1, 0)), _sym(1, 1, h2, center("C2", 1, 1)),
+                          _final(1, 2)])
     return Workload("C2", "two-filter conjunctive pipeline, 10k tuples, 8 KV heads GQA 4:1, "
                     "head_dim 128, 4 layers, prefix 512, global recall target 0.9",
                     spec, 10_000, variants, 2, plans, bench_n=10_000)
@@ -84,7 +92,7 @@ def c3() -> Workload:
     spec = GenSpec(seed=3, n_layers=2, n_kv_heads=8, gqa=4, head_dim=128, n_q=1,
                    op_classes=[1], op_pi_permille=[300], len_min=256, len_max=4096)
     variants = [(k, c) for c in (1, 2) for k in (1000, 500, 200)]
-    plans = [[_final(0, v)] for v in range(len(variants))]
+    plans = [[_final(0, v, center("C3", 0, v))] for v in range(len(variants))]
     return Workload("C3", "100k documents, variable prefix 256-4096 in 16-token pages, sweep of "
                     "prefix/layer-cut variants", spec, 100_000, variants, 3, plans,
                     bench_n=10_000)     # 1.13 TB total: resident batches of 10 k docs (~113 GB)
@@ -94,8 +102,9 @@ def c4() -> Workload:
     spec = GenSpec(seed=4, n_layers=2, n_kv_heads=8, gqa=4, head_dim=128, n_q=1,
                    op_classes=[1, 4, 1], op_pi_permille=[500, 500, 500], len_min=128, len_max=128)
     variants = [(500, 1), (1000, 2)]
-    plans = [[_sym(0, 0, 1.0), _final(0, 1), (1, 0, 2.0, 2.0, 0), _final(1, 1),
-              _sym(2, 0, 1.0), _final(2, 1)]]
+    cm = max(center("C4", 1, 0), 0.0)
+    plans = [[_sym(0, 0, 1.0, center("C4", 0, 0)), _final(0, 1), (1, 0, cm, cm, 0), _final(1, 1),
+              _sym(2, 0, 1.0, center("C4", 2, 0)), _final(2, 1)]]
     return Workload("C4", "three-operator pipeline filter->map-classify->filter, small->large "
                     "cascades, 1M tuples", spec, 1_000_000, variants, 1, plans, mode="routed",
                     bench_n=125_000)    # 1M sharded over 8 GPUs = 125 k per GPU (~131 GB)
@@ -109,7 +118,8 @@ def c5() -> Workload:
     plans = []
     for v1, h1 in per_op:
         for v2, h2 in per_op:
-            plans.append([_sym(0, v1, h1), _final(0, 0), _sym(1, v2, h2), _final(1, 0)])
+            plans.append([_sym(0, v1, h1, center("C5", 0, v1)), _final(0, 0),
+                          _sym(1, v2, h2, center("C5", 1, v2)), _final(1, 0)])
     return Workload("C5", "per-pipeline recall/cost statistics over a 50k labelled sample for a "
                     "64-point threshold/variant grid", spec, 50_000, variants, 0, plans,
                     bench_n=50_000)

@@ -15,7 +15,8 @@ from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libko.so")
+# KO_LIB: alternative build of the same ABI (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("KO_LIB") or os.path.join(_HERE, "lib", "libko.so")
 
 PAGE_TOKENS = 16
 MAX_OPS, MAX_VARIANTS, MAX_STAGES, MAX_PLANS, MAX_CLASSES, MAX_ROWS = 4, 8, 8, 64, 8, 16

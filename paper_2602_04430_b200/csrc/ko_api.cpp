@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -118,22 +119,25 @@ ko_status validate_plan(const ko_plan* P, int g, const int32_t* n_classes, int32
 struct Workspace {
   unsigned long long* unit_counter;
   unsigned long long* worklist_len;
+  unsigned long long* round_len;  // [KO_MAX_VARIANTS] worklist lengths of the routed rounds
   int32_t* done;
   float* part;
   uint4* qfrag;
   uint4* wfrag;
   uint32_t* tuple_state;
   int32_t* worklist;
+  int32_t* round_wl;              // [KO_MAX_VARIANTS][n_tuples]
   size_t total;
 };
 
-// Layout: [counters 256 B][done][part][qfrag][wfrag][tuple_state][worklist]
+// Layout: [counters 256 B][done][part][qfrag][wfrag][tuple_state][worklist][round worklists]
 Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_variants,
                  int64_t n_work, uint8_t* base) {
   Workspace w{};
   const int CPR = pow2_at_least(max_cls);
   const int KS = kv->head_dim / 16;
   const int NT = 2 * CPR;
+  const size_t nt = (size_t)std::max<int64_t>(kv->n_tuples, 1);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -143,13 +147,15 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_va
   uint8_t* ctr = take(256);
   w.unit_counter = (unsigned long long*)ctr;
   w.worklist_len = ctr ? (unsigned long long*)(ctr + 8) : nullptr;
+  w.round_len = ctr ? (unsigned long long*)(ctr + 64) : nullptr;
   w.done = (int32_t*)take(sizeof(int32_t) * (size_t)std::max<int64_t>(n_work, 1));
   w.part = (float*)take(sizeof(float) * (size_t)std::max<int64_t>(n_work, 1) * kv->n_layers *
                         kv->n_kv_heads * n_ops * n_variants * CPR);
   w.qfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * KS * 32);
   w.wfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * NT * KS * 32);
-  w.tuple_state = (uint32_t*)take(sizeof(uint32_t) * (size_t)std::max<int64_t>(kv->n_tuples, 1));
-  w.worklist = (int32_t*)take(sizeof(int32_t) * (size_t)std::max<int64_t>(kv->n_tuples, 1));
+  w.tuple_state = (uint32_t*)take(sizeof(uint32_t) * nt);
+  w.worklist = (int32_t*)take(sizeof(int32_t) * nt);
+  w.round_wl = (int32_t*)take(sizeof(int32_t) * nt * KO_MAX_VARIANTS);
   w.total = off;
   return w;
 }
@@ -191,11 +197,14 @@ ko_status make_tmap(CUtensorMap* map, const ko_kv_cache* kv) {
   return KO_OK;
 }
 
-// fill the kv/op/variant part of ScoreParams and the matching PrepParams for a set of local ops
+// Fill the kv/op/variant part of ScoreParams and the matching PrepParams for the selected ops
+// (caller indices op_sel[0..n_sel)) and variants.  Row slots: the selected ops are laid out in
+// descending class count, n_q·gqa rows each, slot = half·8 + g; CPR0 / CPR1 (returned) are the
+// power-of-two class counts of the two halves of the 16-row tile (CPR1 = 0: one half used).
 void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
                  const ko_operator* ops, const int* op_sel, int n_sel, const ko_variant* variants,
                  const int* var_sel, int n_vsel, int32_t n_ops_total, int32_t n_var_total,
-                 const Workspace& ws, int CPR, int NH) {
+                 const Workspace& ws, int* CPR0, int* CPR1) {
   std::memset(&sp, 0, sizeof(sp));
   std::memset(&pp, 0, sizeof(pp));
   sp.pool = (const uint16_t*)kv->kv_pool;
@@ -212,25 +221,44 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   sp.rows_per_op = kv->gqa_group * kv->n_q;
   sp.n_ops_total = n_ops_total;
   sp.n_var_total = n_var_total;
+  for (int o = 0; o < n_ops_total; ++o) sp.op_classes_g[o] = ops[o].n_classes;
   int n_l = 1;
   sp.n_var = n_vsel;
+  for (int i = 0; i < KO_MAX_VARIANTS; ++i) sp.var_local[i] = -1;
   for (int i = 0; i < n_vsel; ++i) {
     const ko_variant& v = variants[var_sel[i]];
     sp.keep[i] = v.keep_permille;
     sp.cut[i] = v.layer_cut;
     sp.var_ids[i] = var_sel[i];
+    sp.var_local[var_sel[i]] = i;
     n_l = std::max(n_l, (int)v.layer_cut);
   }
   sp.n_l = n_l;
+  // local op order: descending class count (stable)
+  int order[KO_MAX_OPS];
+  for (int i = 0; i < n_sel; ++i) order[i] = op_sel[i];
+  std::stable_sort(order, order + n_sel,
+                   [&](int a, int b) { return ops[a].n_classes > ops[b].n_classes; });
+  int half_cls[2] = {0, 0};
+  for (int r = 0; r < 16; ++r) { sp.slot_op[r] = -1; pp.slot_op[r] = -1; pp.slot_rem[r] = 0; }
+  int slot = 0;
   for (int i = 0; i < n_sel; ++i) {
-    const ko_operator& op = ops[op_sel[i]];
-    sp.op_ids[i] = op_sel[i];
+    const ko_operator& op = ops[order[i]];
+    sp.op_ids[i] = order[i];
     sp.op_classes[i] = op.n_classes;
     sp.bias[i] = op.b;
     pp.q[i] = (const uint16_t*)op.q;
     pp.w[i] = op.w;
     pp.op_classes[i] = op.n_classes;
+    for (int r = 0; r < sp.rows_per_op; ++r, ++slot) {
+      sp.slot_op[slot] = i;
+      pp.slot_op[slot] = i;
+      pp.slot_rem[slot] = r;
+      half_cls[slot / 8] = std::max(half_cls[slot / 8], (int)op.n_classes);
+    }
   }
+  *CPR0 = pow2_at_least(std::max(half_cls[0], 1));
+  *CPR1 = half_cls[1] ? pow2_at_least(half_cls[1]) : 0;
   sp.qfrag = ws.qfrag;
   sp.wfrag = ws.wfrag;
   sp.part = ws.part;
@@ -245,8 +273,8 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   pp.head_dim = kv->head_dim;
   pp.n_ops = n_sel;
   pp.rows_per_op = sp.rows_per_op;
-  pp.NH = NH;
-  pp.CPR = CPR;
+  pp.CPR0 = *CPR0;
+  pp.CPR1 = *CPR1;
   pp.qfrag = ws.qfrag;
   pp.wfrag = ws.wfrag;
 }
@@ -309,13 +337,11 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     int op_sel[KO_MAX_OPS], var_sel[KO_MAX_VARIANTS];
     for (int i = 0; i < n_ops; ++i) op_sel[i] = i;
     for (int i = 0; i < n_variants; ++i) var_sel[i] = i;
-    const int R = n_ops * kv->gqa_group * kv->n_q;
-    const int NH = R > 8 ? 2 : 1;
-    const int CPR = pow2_at_least(maxc);
+    int CPR0 = 1, CPR1 = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
     fill_common(sp, pp, kv, ops, op_sel, n_ops, variants, var_sel, n_variants, n_ops, n_variants,
-                ws, CPR, NH);
+                ws, &CPR0, &CPR1);
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
     sp.work = tuple_idx;
     sp.work_len_host = n_work;
@@ -331,16 +357,15 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_CUDA(ko::launch_score(sp, kv->head_dim, NH, CPR, n_work * sp.n_l * kv->n_kv_heads, s));
+    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end) KO_CUDA(cudaEventRecord(g_trace_end, s));
     return KO_OK;
   }
 
-  // ---- routed mode: the plan's stages in order; each stage scores only the tuples reaching it
+  // ---- routed mode (cascade execution): only tuples reaching a stage are scored
   const ko_plan& P = plans[0];
   if (margins)
     KO_CUDA(cudaMemsetAsync(margins, 0xFF, sizeof(float) * (size_t)n_ops * n_variants * kv->n_tuples, s));
-  KO_CUDA(ko::launch_route_init(ws.tuple_state, kv->n_tuples, s));
   ko::RouteParams rp;
   std::memset(&rp, 0, sizeof(rp));
   rp.plan = P;
@@ -355,18 +380,86 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   rp.worklist_len = ws.worklist_len;
   rp.gold = gold;
   rp.counts = (unsigned long long*)counts;
+
+  // referenced ops and the plan's distinct variants, ordered by extent (keep‰ · layers)
+  int ref_ops[KO_MAX_OPS], n_ref = 0;
+  bool seen_op[KO_MAX_OPS] = {false, false, false, false};
+  int pv[KO_MAX_VARIANTS], n_pv = 0;
+  bool seen_v[KO_MAX_VARIANTS] = {false};
+  for (int i = 0; i < P.n_stages; ++i) {
+    const ko_stage& stg = P.stage[i];
+    if (!seen_op[stg.op]) { seen_op[stg.op] = true; ref_ops[n_ref++] = stg.op; }
+    if (!seen_v[stg.variant]) { seen_v[stg.variant] = true; pv[n_pv++] = stg.variant; }
+  }
+  std::stable_sort(pv, pv + n_pv, [&](int a, int b) {
+    const int64_t ea = (int64_t)variants[a].keep_permille * variants[a].layer_cut;
+    const int64_t eb = (int64_t)variants[b].keep_permille * variants[b].layer_cut;
+    return ea < eb;
+  });
+  // classes per half of the fused row tile decide the W·V tile count; fused rounds pay off while
+  // that stays small (filters), otherwise each stage scores only its own op's rows
+  int max_ref_cls = 1;
+  for (int i = 0; i < n_ref; ++i) max_ref_cls = std::max(max_ref_cls, (int)ops[ref_ops[i]].n_classes);
+  if ((int64_t)n_ref * kv->gqa_group * kv->n_q <= KO_MAX_ROWS && max_ref_cls == 1) {
+    // Rounds of growing extent.  Round r reads each of its tuples ONCE up to the extent of the
+    // r-th variant, scores every referenced op at every variant so far (FLOPs, not bytes), and
+    // walks the plan per tuple as far as those margins allow; a tuple that reaches a stage whose
+    // variant is larger is queued for that variant's round.  Nested prefixes ⇒ each round's read
+    // serves all smaller variants.
+    KO_CUDA(cudaMemsetAsync(ws.round_len, 0, sizeof(unsigned long long) * KO_MAX_VARIANTS, s));
+    for (int r = 0; r < n_pv; ++r) {
+      int CPR0 = 1, CPR1 = 0;
+      ko::ScoreParams sp;
+      ko::PrepParams pp;
+      fill_common(sp, pp, kv, ops, ref_ops, n_ref, variants, pv, r + 1, n_ops, n_variants, ws,
+                  &CPR0, &CPR1);
+      if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
+      for (int k = 0; k < n_pv; ++k) {
+        sp.var_round[pv[k]] = k;
+        sp.wl[k] = ws.round_wl + (size_t)k * std::max<int64_t>(kv->n_tuples, 1);
+        sp.wl_len[k] = ws.round_len + k;
+      }
+      if (r == 0) {
+        sp.work = tuple_idx;
+        sp.work_len_host = n_work;
+        sp.work_len_dev = nullptr;
+      } else {
+        sp.work = sp.wl[r];
+        sp.work_len_host = 0;
+        sp.work_len_dev = (const int64_t*)sp.wl_len[r];
+      }
+      sp.round = r;
+      sp.margins = margins;
+      sp.classes = classes;
+      sp.mode = ko::MODE_WALK;
+      sp.n_plans = 1;
+      sp.plans[0] = P;
+      sp.tuple_state = ws.tuple_state;
+      sp.counts = (unsigned long long*)counts;
+      KO_CUDA(ko::launch_prep(pp, s));
+      KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
+      KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
+      if (g_trace_begin && r == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
+      KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, n_work * sp.n_l * kv->n_kv_heads, s));
+      if (g_trace_end && r + 1 == n_pv) KO_CUDA(cudaEventRecord(g_trace_end, s));
+    }
+    KO_CUDA(ko::launch_final_counts(rp, s));
+    return KO_OK;
+  }
+
+  // fallback: the plan's ops do not fit one 16-row tile — one launch per stage
+  KO_CUDA(ko::launch_route_init(ws.tuple_state, kv->n_tuples, s));
   for (int s_i = 0; s_i < P.n_stages; ++s_i) {
     const ko_stage& stg = P.stage[s_i];
     rp.stage = s_i;
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));  // unit counter + worklist length
     KO_CUDA(ko::launch_route_reach(rp, s));
     int op_sel[1] = {stg.op}, var_sel[1] = {stg.variant};
-    const int R = kv->gqa_group * kv->n_q;
-    const int NH = R > 8 ? 2 : 1;
-    const int CPR = pow2_at_least(ops[stg.op].n_classes);
+    int CPR0 = 1, CPR1 = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
-    fill_common(sp, pp, kv, ops, op_sel, 1, variants, var_sel, 1, n_ops, n_variants, ws, CPR, NH);
+    fill_common(sp, pp, kv, ops, op_sel, 1, variants, var_sel, 1, n_ops, n_variants, ws, &CPR0,
+                &CPR1);
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
     sp.work = ws.worklist;
     sp.work_len_host = 0;
@@ -382,7 +475,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     KO_CUDA(ko::launch_prep(pp, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin && s_i == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_CUDA(ko::launch_score(sp, kv->head_dim, NH, CPR, n_work * sp.n_l * kv->n_kv_heads, s));
+    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end && s_i + 1 == P.n_stages) KO_CUDA(cudaEventRecord(g_trace_end, s));
   }
   KO_CUDA(ko::launch_final_counts(rp, s));

@@ -18,7 +18,7 @@ constexpr int kMaxPlans = KO_MAX_PLANS;
 constexpr int kCountsPerPlan = KO_COUNTS_PER_PLAN;
 constexpr int kThreads = 128;  // score kernel CTA size (4 warps, one work unit per warp)
 
-enum Mode : int32_t { MODE_GRID = 0, MODE_STAGE = 1 };
+enum Mode : int32_t { MODE_GRID = 0, MODE_STAGE = 1, MODE_WALK = 2 };
 
 // One launch of the scoring kernel.  "Local" op/variant indices are positions in this launch;
 // op_ids / var_ids map them to the caller's indices (margins layout, plans, gold).
@@ -42,9 +42,11 @@ struct ScoreParams {
   // operators of this launch
   int32_t n_ops;
   int32_t op_ids[kMaxOps];
-  int32_t op_classes[kMaxOps];
+  int32_t op_classes[kMaxOps];    // by local op
+  int32_t op_classes_g[kMaxOps];  // by caller's op index
   const float* bias[kMaxOps];  // device fp32 [n_classes] per op
   int32_t rows_per_op;  // gqa * n_q
+  int32_t slot_op[16];  // row slot (half*8 + g) → local op, -1 = padding
   int32_t n_ops_total, n_var_total;
   // variants of this launch
   int32_t n_var;
@@ -68,12 +70,20 @@ struct ScoreParams {
   // stage mode: apply plan stage `stage_idx` of `plan` (routed execution)
   int32_t stage_idx;
   uint32_t* tuple_state;
+  // walk mode (routed execution by rounds of nested extents): plan walk per tuple
+  int32_t round;
+  int32_t var_local[kMaxVar];  // caller's variant → local index in this launch, -1 = later round
+  int32_t var_round[kMaxVar];  // caller's variant → round that first computes it
+  int32_t* wl[kMaxVar];                 // per-round worklists
+  unsigned long long* wl_len[kMaxVar];  // their lengths (device)
   ko_plan plans[kMaxPlans];
 };
 
 struct PrepParams {
   int32_t n_l, n_kv_heads, gqa, n_q, n_layers, head_dim;
-  int32_t n_ops, rows_per_op, NH, CPR;
+  int32_t n_ops, rows_per_op, CPR0, CPR1;
+  int32_t slot_op[16];   // row slot → local op (-1 = padding)
+  int32_t slot_rem[16];  // row slot → row within the op (gqa member * n_q + query row)
   const uint16_t* q[kMaxOps];
   const float* w[kMaxOps];
   int32_t op_classes[kMaxOps];
@@ -112,7 +122,7 @@ struct ReduceParams {
 
 // launchers (ko_kernels.cu); return cudaSuccess or the launch error
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
-cudaError_t launch_score(const ScoreParams& p, int head_dim, int NH, int CPR, int64_t max_units,
+cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, int64_t max_units,
                          cudaStream_t s);
 cudaError_t launch_route_reach(const RouteParams& p, cudaStream_t s);  // build worklist for stage
 cudaError_t launch_route_apply(const RouteParams& p, cudaStream_t s);  // apply stage on margins

@@ -1,6 +1,6 @@
 // ko_kernels.cu — sm_100a kernels of the KV-cache semantic-operator scoring pass.
 //
-// Hot kernel: ko_score_kernel<D, NH, CPR>.  One warp owns one work unit = (tuple t, layer l,
+// Hot kernel: ko_score_kernel<D, CPR0, CPR1>.  One warp owns one work unit = (tuple t, layer l,
 // kv-head h) and streams that unit's K and V rows (importance order, page by page) straight from
 // HBM with 128-bit non-allocating loads, one page ahead.  Per 16-token page:
 //   S = Q · Kᵀ        on tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate): the rows
@@ -185,11 +185,16 @@ struct Ring {
   static constexpr int kSmemBytes = (kThreads / 32) * kWarpBytes + 1024;  // + alignment slack
 };
 
-template <int D, int NH, int CPR>
+// CPR0 / CPR1: classes per row slot in half 0 (A rows g) / half 1 (A rows g+8) of the row tile;
+// CPR1 = 0 when at most 8 rows attend a kv-head.  W·V tiles: CPR0 + CPR1 (half h, class c →
+// tile h ? CPR0 + c : c); partial logits are stored with stride CPR = CPR0 (≥ every op's classes).
+template <int D, int CPR0, int CPR1>
 __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_constant__ ScoreParams p) {
   constexpr int KS = D / 16;  // mma k-steps over head_dim
   constexpr int KP = D / 32;  // 128-bit fragment reads per token row per lane (2 k-steps each)
-  constexpr int NT = NH * CPR;
+  constexpr int NH = CPR1 > 0 ? 2 : 1;
+  constexpr int CPR = CPR0;
+  constexpr int NT = CPR0 + CPR1;
   constexpr int S = Ring<D>::kStages;
   constexpr int STAGE = Ring<D>::kStageBytes;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   uint8_t* ring = ring_base + warp * Ring<D>::kWarpBytes;
   const uint32_t ring_s = smem_u32(ring);
 
-  const int n_cnt_rows = p.mode == MODE_GRID ? p.n_plans : (p.tuple_state ? 1 : 0);
+  const int n_cnt_rows = p.mode == MODE_GRID ? p.n_plans : (p.tuple_state ? 1 : 0);  // stage/walk: row 0
   for (int i = threadIdx.x; i < n_cnt_rows * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&s_full[warp][s], 1);
@@ -222,17 +227,15 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 
   const int64_t n_work = p.work_len_dev ? *p.work_len_dev : p.work_len_host;
   const int Hkv = p.n_kv_heads;
-  const int upt = p.n_l * Hkv;  // units per tuple
+  const int upt = p.n_l * Hkv;  // work units per tuple: one per (layer, kv-head)
   const int64_t n_units = n_work * upt;
   const int R = p.n_ops * p.rows_per_op;
 
   // row slot → local op for this lane's two half-slots
   int slot_op[NH];
 #pragma unroll
-  for (int hs = 0; hs < NH; ++hs) {
-    const int rho = hs * 8 + g;
-    slot_op[hs] = rho < R ? rho / p.rows_per_op : -1;
-  }
+  for (int hs = 0; hs < NH; ++hs) slot_op[hs] = p.slot_op[hs * 8 + g];
+  (void)R;
 
   // lane-constant smem offsets of this lane's fragment reads inside a stage: token row g (+8),
   // d-chunk (2q + (j & 1)) of box (j >> 1), XOR-swizzled by the row (= token mod 8)
@@ -403,8 +406,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
             for (int k = 0; k < 4; ++k) ps[k] = ex2(x[k] - mn);
             sm[hs] = sm[hs] * corr + ((ps[0] + ps[1]) + (ps[2] + ps[3]));
 #pragma unroll
-            for (int c = 0; c < CPR; ++c) {
-              const int tt = hs * CPR + c;
+            for (int c = 0; c < (hs == 0 ? CPR0 : CPR1); ++c) {
+              const int tt = hs == 0 ? c : CPR0 + c;
               float a = ac[hs][c] * corr;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
@@ -431,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
             den += __shfl_xor_sync(0xffffffffu, den, 2);
 #pragma unroll
             for (int c = 0; c < CPR; ++c) {
+              if (c >= (hs == 0 ? CPR0 : CPR1)) { val[hs][c] = 0.f; continue; }
               float a = ac[hs][c] * f;
               a += __shfl_xor_sync(0xffffffffu, a, 1);
               a += __shfl_xor_sync(0xffffffffu, a, 2);
@@ -482,11 +486,16 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     __syncwarp();
     int last = 0;
     if (lane == 0) {
-      __threadfence();
-      last = atomicAdd(p.done + wslot, 1) == upt - 1;
+      // release: this unit's partial logits (stored by this lane) are visible before the count
+      uint32_t prev;
+      asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(prev)
+                   : "l"(p.done + wslot)
+                   : "memory");
+      last = prev == (uint32_t)(upt - 1);
     }
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) continue;
+    if (last) {
     __threadfence();
 
     float* zs = s_z[warp];
@@ -507,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       zs[idx] = zf;
     }
     __syncwarp();
+    const bool walk = p.mode == MODE_WALK;
     for (int idx = lane; idx < p.n_ops * p.n_var; idx += 32) {
       const int o = idx / p.n_var, v = idx % p.n_var;
       const float* zz = zs + idx * CPR;
@@ -522,28 +532,70 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
           if (c != cls && zz[c] > second) second = zz[c];
         m = zz[cls] - second;
       }
-      const size_t oi = ((size_t)p.op_ids[o] * p.n_var_total + p.var_ids[v]) * p.n_tuples + t;
-      if (p.margins) p.margins[oi] = m;
-      if (p.classes) p.classes[oi] = cls;
-      s_m[warp][idx] = m;
-      s_c[warp][idx] = cls;
+      if (!walk) {  // walk mode writes only the entries the plan reaches
+        const size_t oi = ((size_t)p.op_ids[o] * p.n_var_total + p.var_ids[v]) * p.n_tuples + t;
+        if (p.margins) p.margins[oi] = m;
+        if (p.classes) p.classes[oi] = cls;
+      }
+      s_m[warp][p.op_ids[o] * p.n_var + v] = m;  // indexed by the caller's op, local variant
+      s_c[warp][p.op_ids[o] * p.n_var + v] = cls;
     }
     __syncwarp();
     if (p.mode == MODE_GRID) {
       for (int gp = lane; gp < p.n_plans; gp += 32)
-        eval_plan(p.plans[gp], s_m[warp], s_c[warp], p.n_var, p.op_classes, p.gold, p.n_tuples, t,
-                  s_cnt + gp * kCountsPerPlan);
+        eval_plan(p.plans[gp], s_m[warp], s_c[warp], p.n_var, p.op_classes_g, p.gold, p.n_tuples,
+                  t, s_cnt + gp * kCountsPerPlan);
+    } else if (walk) {
+      if (lane == 0) {
+        // routed execution: walk the plan from where the tuple stopped, deciding every stage
+        // whose variant this round computed (Eqs. accept-i/reject-i/unsure-i)
+        const ko_plan& P = p.plans[0];
+        uint32_t state = p.round == 0 ? 1u : p.tuple_state[t];
+        int s = (int)((state >> 24) & 15u);
+        for (; s < P.n_stages; ++s) {
+          const ko_stage& st = P.stage[s];
+          const int o = st.op;
+          if (!(state & 1u) || op_status(state, o) != 0) continue;  // not reached
+          const int vl = p.var_local[st.variant];
+          if (vl < 0) {  // its variant's extent comes in a later round
+            const int r = p.var_round[st.variant];
+            const unsigned long long pos = atomicAdd(p.wl_len[r], 1ull);
+            p.wl[r][pos] = (int32_t)t;
+            break;
+          }
+          const float m = s_m[warp][o * p.n_var + vl];
+          const int32_t cls = s_c[warp][o * p.n_var + vl];
+          const size_t oi = ((size_t)o * p.n_var_total + st.variant) * p.n_tuples + t;
+          if (p.margins) p.margins[oi] = m;
+          if (p.classes) p.classes[oi] = cls;
+          int* cnt = s_cnt + 5 + 4 * s;
+          atomicAdd(&cnt[0], 1);
+          const int d = decide(m, st, p.op_classes_g[o]);
+          if (d == D_ACCEPT || d == D_RESOLVED) {
+            state |= 1u << (1 + 2 * o);
+            if (d == D_RESOLVED) state |= ((uint32_t)cls & 15u) << (16 + 4 * o);
+            atomicAdd(&cnt[1], 1);
+          } else if (d == D_REJECT) {
+            state = (state & ~1u) | (2u << (1 + 2 * o));
+            atomicAdd(&cnt[2], 1);
+          } else {
+            atomicAdd(&cnt[3], 1);
+          }
+        }
+        p.tuple_state[t] = (state & ~(15u << 24)) | ((uint32_t)s << 24);
+      }
     } else if (lane == 0 && p.tuple_state) {
-      // routed execution: apply stage `stage_idx` (this launch has exactly its op and variant)
+      // routed execution, one stage per launch (fallback when the plan's ops do not fit one
+      // row tile): apply stage `stage_idx` (this launch has exactly its op and variant)
       const ko_stage& st = p.plans[0].stage[p.stage_idx];
       const int o = st.op;
-      const int d = decide(s_m[warp][0], st, p.op_classes[0]);
+      const int d = decide(s_m[warp][o * p.n_var + 0], st, p.op_classes[0]);
       uint32_t state = p.tuple_state[t];
       int* cnt = s_cnt + 5 + 4 * p.stage_idx;
       atomicAdd(&cnt[0], 1);
       if (d == D_ACCEPT || d == D_RESOLVED) {
         state |= 1u << (1 + 2 * o);
-        if (d == D_RESOLVED) state |= ((uint32_t)s_c[warp][0] & 15u) << (16 + 4 * o);
+        if (d == D_RESOLVED) state |= ((uint32_t)s_c[warp][o * p.n_var + 0] & 15u) << (16 + 4 * o);
         atomicAdd(&cnt[1], 1);
       } else if (d == D_REJECT) {
         state = (state & ~1u) | (2u << (1 + 2 * o));
@@ -553,6 +605,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       }
       p.tuple_state[t] = state;
     }
+    }  // last
   }
   if (n_cnt_rows) flush_counts(s_cnt, n_cnt_rows, p.counts);
 }
@@ -571,9 +624,8 @@ __device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) {
 
 __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
   const int KS = p.head_dim / 16;
-  const int NT = p.NH * p.CPR;
+  const int NT = p.CPR0 + p.CPR1;
   const int Hq = p.n_kv_heads * p.gqa;
-  const int R = p.n_ops * p.rows_per_op;
   const int n_lh = p.n_l * p.n_kv_heads;
   const int64_t nq_items = (int64_t)n_lh * KS * 32;
   const int64_t nw_items = (int64_t)n_lh * NT * KS * 32;
@@ -596,8 +648,8 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
         const int rho = hr * 8 + g;
         for (int k = 0; k < 4; ++k) {
           uint16_t b = 0;
-          if (rho < R) {
-            const int o = rho / p.rows_per_op, rem = rho % p.rows_per_op;
+          if (p.slot_op[rho] >= 0) {
+            const int o = p.slot_op[rho], rem = p.slot_rem[rho];
             const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
             b = p.q[o][(((size_t)l * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k];
           }
@@ -605,12 +657,12 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
         }
       }
     } else {
-      const int hs = tt / p.CPR, c = tt % p.CPR;
+      const int hs = tt < p.CPR0 ? 0 : 1, c = tt < p.CPR0 ? tt : tt - p.CPR0;
       const int rho = hs * 8 + g;
       for (int k = 0; k < 4; ++k) {
         float w = 0.f;
-        if (rho < R) {
-          const int o = rho / p.rows_per_op, rem = rho % p.rows_per_op;
+        if (p.slot_op[rho] >= 0) {
+          const int o = p.slot_op[rho], rem = p.slot_rem[rho];
           const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
           if (c < p.op_classes[o])
             w = p.w[o][((((size_t)c * p.n_layers + l) * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k];
@@ -804,14 +856,14 @@ int num_sms() {
   return n;
 }
 
-template <int D, int NH, int CPR>
+template <int D, int CPR0, int CPR1>
 cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t s) {
   static int occ = 0;
   constexpr int smem = Ring<D>::kSmemBytes;
   if (!occ) {
-    cudaFuncSetAttribute(ko_score_kernel<D, NH, CPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(ko_score_kernel<D, CPR0, CPR1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ko_score_kernel<D, NH, CPR>, kThreads,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ko_score_kernel<D, CPR0, CPR1>, kThreads,
                                                   smem);
     if (occ < 1) occ = 1;
   }
@@ -820,7 +872,7 @@ cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t
   const int64_t need = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  ko_score_kernel<D, NH, CPR><<<(unsigned)grid, kThreads, smem, s>>>(p);
+  ko_score_kernel<D, CPR0, CPR1><<<(unsigned)grid, kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -831,13 +883,15 @@ cudaError_t launch_prep(const PrepParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_score(const ScoreParams& p, int head_dim, int NH, int CPR, int64_t max_units,
+cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, int64_t max_units,
                          cudaStream_t s) {
-#define KO_DISPATCH(DD, HH, CC) \
-  if (head_dim == DD && NH == HH && CPR == CC) return launch_score_t<DD, HH, CC>(p, max_units, s);
-#define KO_DISPATCH_D(DD)                                                          \
-  KO_DISPATCH(DD, 1, 1) KO_DISPATCH(DD, 1, 2) KO_DISPATCH(DD, 1, 4) KO_DISPATCH(DD, 1, 8) \
-  KO_DISPATCH(DD, 2, 1) KO_DISPATCH(DD, 2, 2) KO_DISPATCH(DD, 2, 4) KO_DISPATCH(DD, 2, 8)
+#define KO_DISPATCH(DD, C0, C1) \
+  if (head_dim == DD && CPR0 == C0 && CPR1 == C1) return launch_score_t<DD, C0, C1>(p, max_units, s);
+#define KO_DISPATCH_D(DD)                                                                  \
+  KO_DISPATCH(DD, 1, 0) KO_DISPATCH(DD, 1, 1) KO_DISPATCH(DD, 2, 0) KO_DISPATCH(DD, 2, 1)   \
+  KO_DISPATCH(DD, 2, 2) KO_DISPATCH(DD, 4, 0) KO_DISPATCH(DD, 4, 1) KO_DISPATCH(DD, 4, 2)   \
+  KO_DISPATCH(DD, 4, 4) KO_DISPATCH(DD, 8, 0) KO_DISPATCH(DD, 8, 1) KO_DISPATCH(DD, 8, 2)   \
+  KO_DISPATCH(DD, 8, 4) KO_DISPATCH(DD, 8, 8)
   KO_DISPATCH_D(64)
   KO_DISPATCH_D(128)
 #undef KO_DISPATCH_D

@@ -205,3 +205,44 @@ def test_error_paths(ko):
     ws = torch.empty(64, dtype=torch.uint8, device="cuda")
     with pytest.raises(ko.KoError, match="workspace"):
         ko.score_batch(d["kv"], d["ops"], wl.variants, workspace=ws)
+
+
+def test_routed_rounds_c2_plan(ko):
+    """Routed execution by rounds of nested extents on a 2-filter, 3-variant cascade plan."""
+    wl = workloads.get("C2")
+    n = 600
+    d = device_workload(wl, n=n)
+    plan = wl.plans[5]
+    m, c, counts = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan], gold=d["gold"])
+    _, _, grid = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan, plan], gold=d["gold"])
+    torch.cuda.synchronize()
+    m_or, c_or = oracle.score_workload(wl, np.arange(n))
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    reached = np.isfinite(mg)
+    assert reached[0, 0].all()                       # every tuple meets the first stage
+    assert not reached.all()                         # ... and the cascade skips work
+    parity.assert_margins(mg, m_or, mask=reached)
+    parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], wl.spec.op_classes,
+                         d["gold"].cpu().numpy())
+    assert np.array_equal(grid.cpu().numpy()[0], counts.cpu().numpy()[0])
+
+
+def test_routed_fallback_many_rows(ko):
+    """Plans whose ops need > 16 rows per kv-head run one launch per stage (fallback path)."""
+    geom = Geom(2, 1, 4, 64, 2)                      # 8 rows per op, 3 ops = 24 rows
+    rng = np.random.default_rng(11)
+    lengths = [5, 40, 64, 90, 17, 33]
+    K, V, ops_h = random_problem(rng, geom, lengths, n_ops=3, classes=(1, 3, 1))
+    pool, indptr, ids, sl = build_pool(K, V, lengths, poison=True)
+    variants = [(400, 1), (1000, 2)]
+    plan = [(0, 0, -0.05, 0.05, 0), (0, 1, 0.0, 0.0, 1), (1, 0, 0.1, 0.1, 0), (1, 1, 0.0, 0.0, 1),
+            (2, 1, 0.0, 0.0, 1)]
+    m_or, c_or = oracle.score(geom, pool, indptr, ids, sl, ops_h, variants)
+    gold = np.stack([(m_or[0, 1] > 0), c_or[1, 1], (m_or[2, 1] > 0)]).astype(np.uint8)
+    kv, ops = tensors_to_device(pool, indptr, ids, sl, geom, ops_h)
+    m, c, counts = ko.score_batch(kv, ops, variants, plans=[plan],
+                                  gold=torch.from_numpy(gold).cuda())
+    torch.cuda.synchronize()
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    parity.assert_margins(mg, m_or, mask=np.isfinite(mg))
+    parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], [1, 3, 1], gold)
