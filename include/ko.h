@@ -178,6 +178,24 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
                           int32_t n_variants, int64_t n_tuples, const uint8_t* gold,
                           int64_t* counts, void* stream);
 
+/* ko_soft_stats — the continuous relaxation of one plan (NEXT-1 of SURVEY §8(f)) on
+ * precomputed margins: pick factors σ_i = sigmoid(s_i/τ) (final stages σ = 1), soft decisions
+ * π_i = softmax([m − θ⁺, θ⁻ − m, 0]/τ) (final stages: accept = sigmoid((m − θ⁺)/τ)), the relaxed
+ * recurrences of Eqs. accept-i / reject-i / unsure-i, plan accept mass = product over the plan's
+ * operators, soft TP / FP / FN (Eqs. 5–7) and cost Σ σ_i c_i · (mass reaching stage i) — and the
+ * exact derivatives of these four sums w.r.t. every stage's (s_i, θ⁻_i, θ⁺_i) at the plan's
+ * thresholds.  Filter operators only (maps: KO_EUNSUPPORTED).
+ * pick_scores, stage_cost: HOST double [plan->n_stages]; tau > 0; n_classes: host [n_ops].
+ * out: DEVICE double [4 + 12·n_stages] = {TP, FP, FN, cost} then, for q in (TP, FP, FN, cost),
+ *      d q / d(s_i, θ⁻_i, θ⁺_i) at index 4 + q·3·n_stages + 3i + {0,1,2} (finals: d/ds = d/dθ⁻ = 0,
+ *      the threshold derivative is reported on θ⁺).  Sums are fp64 in a fixed order
+ *      (bitwise reproducible).  workspace: >= ko_soft_workspace_size(n_stages, n_tuples) bytes. */
+ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const double* stage_cost,
+                        double tau, const float* margins, const int32_t* n_classes, int32_t n_ops,
+                        int32_t n_variants, int64_t n_tuples, const uint8_t* gold, double* out,
+                        void* workspace, size_t workspace_bytes, void* stream);
+size_t ko_soft_workspace_size(int32_t n_stages, int64_t n_tuples);
+
 /* Bytes of device workspace ko_score_batch needs for this shape (n_work = number of tuples it
  * will process: n_idx, or n_tuples when tuple_idx is NULL).  Returns 0 on invalid arguments. */
 size_t ko_workspace_size(const ko_kv_cache* kv, const ko_operator* ops, int32_t n_ops,

@@ -75,6 +75,11 @@ def _load():
     L.ko_workspace_size.restype = ctypes.c_size_t
     L.ko_beta_lower_bound.argtypes = [I64, I64, ctypes.c_double]
     L.ko_beta_lower_bound.restype = ctypes.c_double
+    L.ko_soft_stats.argtypes = [P, P, P, ctypes.c_double, P, P, I32, I32, I64, P, P, P,
+                                ctypes.c_size_t, P]
+    L.ko_soft_stats.restype = ctypes.c_int
+    L.ko_soft_workspace_size.argtypes = [I32, I64]
+    L.ko_soft_workspace_size.restype = ctypes.c_size_t
     L.ko_set_trace_events.argtypes = [P, P]
     L.ko_set_trace_events.restype = None
     L.ko_last_error.restype = ctypes.c_char_p
@@ -84,7 +89,8 @@ def _load():
 
 _lib = _load()
 EXPORTS = ("ko_score_batch", "ko_route", "ko_reduce_stats", "ko_workspace_size",
-           "ko_beta_lower_bound", "ko_set_trace_events", "ko_last_error", "ko_version")
+           "ko_soft_stats", "ko_soft_workspace_size", "ko_beta_lower_bound",
+           "ko_set_trace_events", "ko_last_error", "ko_version")
 
 
 def lib():
@@ -257,6 +263,29 @@ def reduce_stats(plans: Sequence[Sequence[Stage]], margins, classes, n_classes: 
                               nc, n_ops, n_var, n, _ptr(gold), counts.data_ptr(), _stream(stream))
     _check(rc)
     return counts
+
+
+def soft_stats(plan: Sequence[Stage], pick_scores: Sequence[float], stage_cost: Sequence[float],
+               tau: float, margins, n_classes: Sequence[int], gold=None, out=None,
+               workspace=None, stream=None):
+    """ko_soft_stats: relaxed TP/FP/FN/cost and their Jacobian w.r.t. (s_i, θ⁻_i, θ⁺_i).
+    Returns a device fp64 tensor [4 + 12·S] (see include/ko.h for the layout)."""
+    import torch
+    n_ops, n_var, n = margins.shape
+    S = len(plan)
+    if out is None:
+        out = torch.empty(4 + 12 * S, dtype=torch.float64, device=margins.device)
+    if workspace is None:
+        workspace = torch.empty(int(_lib.ko_soft_workspace_size(S, n)), dtype=torch.uint8,
+                                device=margins.device)
+    pk = (ctypes.c_double * S)(*[float(x) for x in pick_scores])
+    cs = (ctypes.c_double * S)(*[float(x) for x in stage_cost])
+    nc = (ctypes.c_int32 * n_ops)(*[int(c) for c in n_classes])
+    rc = _lib.ko_soft_stats(make_plans([plan]), pk, cs, float(tau), margins.data_ptr(), nc, n_ops,
+                            n_var, n, _ptr(gold), out.data_ptr(), workspace.data_ptr(),
+                            workspace.numel(), _stream(stream))
+    _check(rc)
+    return out
 
 
 def set_trace_events(ev_begin=None, ev_end=None) -> None:

@@ -570,6 +570,49 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
   return KO_OK;
 }
 
+size_t ko_soft_workspace_size(int32_t n_stages, int64_t n_tuples) {
+  if (n_stages < 1 || n_stages > KO_MAX_STAGES || n_tuples < 0) return 0;
+  return align256(sizeof(double) * (size_t)(3 * n_stages + 1) * 4 * (size_t)std::max<int64_t>(n_tuples, 1));
+}
+
+ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const double* stage_cost,
+                        double tau, const float* margins, const int32_t* n_classes, int32_t n_ops,
+                        int32_t n_variants, int64_t n_tuples, const uint8_t* gold, double* out,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  if (!plan || !pick_scores || !stage_cost || !margins || !n_classes || !out || !workspace)
+    return fail(KO_EINVAL, "ko_soft_stats: NULL argument");
+  if (n_ops < 1 || n_ops > KO_MAX_OPS) return fail(KO_EINVAL, "n_ops %d", n_ops);
+  if (n_variants < 1 || n_variants > KO_MAX_VARIANTS) return fail(KO_EINVAL, "n_variants %d", n_variants);
+  if (n_tuples < 0) return fail(KO_EINVAL, "n_tuples < 0");
+  if (!(tau > 0.0) || !std::isfinite(tau)) return fail(KO_EINVAL, "tau must be > 0");
+  ko_status st;
+  if ((st = validate_plan(plan, 0, n_classes, n_ops, n_variants)) != KO_OK) return st;
+  ko::SoftParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  for (int i = 0; i < plan->n_stages; ++i) {
+    if (n_classes[plan->stage[i].op] > 1)
+      return fail(KO_EUNSUPPORTED, "ko_soft_stats: stage %d is a map operator (filters only)", i);
+    if (!std::isfinite(pick_scores[i]) || !std::isfinite(stage_cost[i]))
+      return fail(KO_EINVAL, "stage %d: non-finite pick score or cost", i);
+    sp.pick[i] = pick_scores[i];
+    sp.stage_cost[i] = stage_cost[i];
+    sp.referenced[plan->stage[i].op] = 1;
+  }
+  if (workspace_bytes < ko_soft_workspace_size(plan->n_stages, n_tuples))
+    return fail(KO_EWORKSPACE, "workspace %zu < %zu", workspace_bytes,
+                ko_soft_workspace_size(plan->n_stages, n_tuples));
+  sp.plan = *plan;
+  sp.tau = tau;
+  sp.margins = margins;
+  sp.n_ops = n_ops;
+  sp.n_variants = n_variants;
+  sp.n_tuples = n_tuples;
+  sp.gold = gold;
+  sp.items = (double*)workspace;
+  KO_CUDA(ko::launch_soft(sp, out, (cudaStream_t)stream));
+  return KO_OK;
+}
+
 // ---- Bayesian lower bound (host): I^{-1}(1 − α; 1 + a, 1 + b) -------------------------------
 // Regularized incomplete beta by the continued fraction (modified Lentz), inverse by bisection.
 static double betacf(double a, double b, double x) {

@@ -120,6 +120,21 @@ struct ReduceParams {
   ko_plan plans[kMaxPlans];
 };
 
+// soft relaxation of one plan (ko_soft.cu)
+struct SoftParams {
+  ko_plan plan;
+  double pick[KO_MAX_STAGES];
+  double stage_cost[KO_MAX_STAGES];
+  double tau;
+  const float* margins;  // [n_ops][n_variants][n_tuples]
+  int32_t n_ops, n_variants;
+  int64_t n_tuples;
+  const uint8_t* gold;   // [n_ops][n_tuples] or NULL
+  int32_t referenced[kMaxOps];
+  double* items;         // workspace [3·S + 1][4][n_tuples]
+};
+cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s);
+
 // launchers (ko_kernels.cu); return cudaSuccess or the launch error
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
 cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, int64_t max_units,

@@ -1,0 +1,47 @@
+"""GPU parity of ko_soft_stats (NEXT-1) against the oracle (oracle/soft.py, torch fp64 +
+autograd): values and Jacobian to ~1e-9 relative on the same margins."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import soft  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ko():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2602_04430_b200 as ko
+    return ko
+
+
+@pytest.mark.parametrize("tau", [1.0, 0.1, 0.01])
+def test_soft_stats_parity(ko, tau):
+    rng = np.random.default_rng(int(tau * 1000))
+    n = 5000
+    m = rng.normal(0, 2, size=(3, 3, n)).astype(np.float32)
+    gold = (rng.random((3, n)) < 0.5).astype(np.uint8)
+    plan = [(0, 0, -1.0, 0.7, 0), (2, 0, -0.3, 0.2, 0), (0, 1, -0.5, 0.5, 0), (0, 2, 0.0, 0.0, 1),
+            (2, 2, 0.1, 0.1, 1), (1, 1, -0.2, 0.4, 0), (1, 2, -0.25, -0.25, 1)]
+    pick = [0.3, -0.2, 0.1, 0.0, 0.0, 0.05, 0.0]
+    cost = [1.0, 1.5, 3.0, 10.0, 10.0, 2.0, 10.0]
+    exp = soft.soft_stats(plan, pick, tau, m.astype(np.float64), gold, cost)
+    out = ko.soft_stats(plan, pick, cost, tau, torch.from_numpy(m).cuda(), [1, 1, 1],
+                        gold=torch.from_numpy(gold).cuda())
+    got = out.cpu().numpy()
+    S = len(plan)
+    assert np.allclose(got[:4], exp["values"], rtol=1e-10, atol=1e-9)
+    jac = got[4:].reshape(4, 3 * S)
+    scale = np.abs(exp["jacobian"]).max()
+    assert np.allclose(jac, exp["jacobian"], rtol=1e-8, atol=1e-10 * max(scale, 1.0))
+    out2 = ko.soft_stats(plan, pick, cost, tau, torch.from_numpy(m).cuda(), [1, 1, 1],
+                         gold=torch.from_numpy(gold).cuda())
+    assert torch.equal(out, out2)                      # fixed-order sums: bitwise reproducible
+
+
+def test_soft_stats_rejects_maps(ko):
+    m = torch.zeros((1, 1, 4), device="cuda")
+    with pytest.raises(ko.KoError, match="map"):
+        ko.soft_stats([(0, 0, 0.0, 0.0, 1)], [0.0], [1.0], 1.0, m, [3])
