@@ -72,8 +72,11 @@ def soft_stats(plan: Sequence[Tuple], pick: Sequence[float], tau: float, margins
     (final stages: d/ds = 0, the threshold derivative is reported on θ⁺, d/dθ⁻ = 0)."""
     S = len(plan)
     s = torch.tensor([float(x) for x in pick], dtype=torch.float64, requires_grad=True)
-    lo = torch.tensor([st[2] for st in plan], dtype=torch.float64, requires_grad=True)
-    hi = torch.tensor([st[3] for st in plan], dtype=torch.float64, requires_grad=True)
+    # thresholds are fp32 in a plan (ko.h ko_stage): widened exactly, as in the hard oracle
+    lo = torch.tensor([float(np.float32(st[2])) for st in plan], dtype=torch.float64,
+                      requires_grad=True)
+    hi = torch.tensor([float(np.float32(st[3])) for st in plan], dtype=torch.float64,
+                      requires_grad=True)
     mt = torch.from_numpy(np.asarray(margins, np.float64))
     gt = torch.from_numpy(np.asarray(gold, np.float64))
     ct = [float(c) for c in stage_cost]

@@ -400,7 +400,11 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   // that stays small (filters), otherwise each stage scores only its own op's rows
   int max_ref_cls = 1;
   for (int i = 0; i < n_ref; ++i) max_ref_cls = std::max(max_ref_cls, (int)ops[ref_ops[i]].n_classes);
-  if ((int64_t)n_ref * kv->gqa_group * kv->n_q <= KO_MAX_ROWS && max_ref_cls == 1) {
+  static const int force_walk = [] {  // tuning knob (A/B measurements): fuse maps too
+    const char* e = std::getenv("KO_WALK_MAPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if ((int64_t)n_ref * kv->gqa_group * kv->n_q <= KO_MAX_ROWS && (max_ref_cls == 1 || force_walk)) {
     // Rounds of growing extent.  Round r reads each of its tuples ONCE up to the extent of the
     // r-th variant, scores every referenced op at every variant so far (FLOPs, not bytes), and
     // walks the plan per tuple as far as those margins allow; a tuple that reaches a stage whose

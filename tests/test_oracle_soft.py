@@ -85,7 +85,7 @@ def test_gradients_match_finite_differences():
     tau, cost = 0.7, [1.0, 2.0, 3.0, 10.0, 20.0]
     out = soft.soft_stats(plan, pick, tau, m, gold, cost)
     jac = out["jacobian"]
-    eps = 1e-6
+    eps = 2.0 ** -20          # exact in fp32 next to the thresholds (plans carry fp32 θ)
     for i in range(len(plan)):
         for k, field in enumerate(("s", "lo", "hi")):
             if plan[i][4] and field != "hi":
