@@ -126,11 +126,15 @@ struct Workspace {
   uint4* wfrag;
   uint32_t* tuple_state;
   int32_t* worklist;
-  int32_t* round_wl;              // [KO_MAX_VARIANTS][n_tuples]
+  int32_t* round_wl;              // [KO_MAX_STAGES][n_tuples] per-position worklists
+  uint32_t* tuple_done;           // [n_tuples]
+  float* wm;                      // [n_ops][n_variants][n_tuples]
+  int32_t* wc;
   size_t total;
 };
 
-// Layout: [counters 256 B][done][part][qfrag][wfrag][tuple_state][worklist][round worklists]
+// Layout: [counters 256 B][done][part][qfrag][wfrag][tuple_state][worklist][position
+// worklists][tuple_done][wm][wc]
 Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_variants,
                  int64_t n_work, uint8_t* base) {
   Workspace w{};
@@ -155,7 +159,10 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_va
   w.wfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * NT * KS * 32);
   w.tuple_state = (uint32_t*)take(sizeof(uint32_t) * nt);
   w.worklist = (int32_t*)take(sizeof(int32_t) * nt);
-  w.round_wl = (int32_t*)take(sizeof(int32_t) * nt * KO_MAX_VARIANTS);
+  w.round_wl = (int32_t*)take(sizeof(int32_t) * nt * KO_MAX_STAGES);
+  w.tuple_done = (uint32_t*)take(sizeof(uint32_t) * nt);
+  w.wm = (float*)take(sizeof(float) * nt * n_ops * n_variants);
+  w.wc = (int32_t*)take(sizeof(int32_t) * nt * n_ops * n_variants);
   w.total = off;
   return w;
 }
@@ -381,106 +388,89 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   rp.gold = gold;
   rp.counts = (unsigned long long*)counts;
 
-  // referenced ops and the plan's distinct variants, ordered by extent (keep‰ · layers)
-  int ref_ops[KO_MAX_OPS], n_ref = 0;
-  bool seen_op[KO_MAX_OPS] = {false, false, false, false};
+  // Operator groups: the referenced filters fused into row tiles of ≤ 16 rows, each map alone
+  // (a K-class map needs K readout tiles).  Variant ranks: the plan's distinct variants ordered
+  // by extent (keep‰ · layers); a launch of rank r computes every variant of rank ≤ r in one read.
+  const int rows_per_op = kv->gqa_group * kv->n_q;
+  int group_of_op[KO_MAX_OPS] = {-1, -1, -1, -1};
+  int group_ops[KO_MAX_OPS][KO_MAX_OPS], group_n[KO_MAX_OPS] = {0, 0, 0, 0}, n_groups = 0;
+  int filter_group = -1;
+  for (int i = 0; i < P.n_stages; ++i) {
+    const int o = P.stage[i].op;
+    if (group_of_op[o] >= 0) continue;
+    int g;
+    if (ops[o].n_classes <= 1 && filter_group >= 0 &&
+        (group_n[filter_group] + 1) * rows_per_op <= KO_MAX_ROWS) {
+      g = filter_group;
+    } else {
+      g = n_groups++;
+      if (ops[o].n_classes <= 1) filter_group = g;
+    }
+    group_of_op[o] = g;
+    group_ops[g][group_n[g]++] = o;
+  }
   int pv[KO_MAX_VARIANTS], n_pv = 0;
   bool seen_v[KO_MAX_VARIANTS] = {false};
-  for (int i = 0; i < P.n_stages; ++i) {
-    const ko_stage& stg = P.stage[i];
-    if (!seen_op[stg.op]) { seen_op[stg.op] = true; ref_ops[n_ref++] = stg.op; }
-    if (!seen_v[stg.variant]) { seen_v[stg.variant] = true; pv[n_pv++] = stg.variant; }
-  }
+  for (int i = 0; i < P.n_stages; ++i)
+    if (!seen_v[P.stage[i].variant]) { seen_v[P.stage[i].variant] = true; pv[n_pv++] = P.stage[i].variant; }
   std::stable_sort(pv, pv + n_pv, [&](int a, int b) {
     const int64_t ea = (int64_t)variants[a].keep_permille * variants[a].layer_cut;
     const int64_t eb = (int64_t)variants[b].keep_permille * variants[b].layer_cut;
     return ea < eb;
   });
-  // classes per half of the fused row tile decide the W·V tile count; fused rounds pay off while
-  // that stays small (filters), otherwise each stage scores only its own op's rows
-  int max_ref_cls = 1;
-  for (int i = 0; i < n_ref; ++i) max_ref_cls = std::max(max_ref_cls, (int)ops[ref_ops[i]].n_classes);
-  static const int force_walk = [] {  // tuning knob (A/B measurements): fuse maps too
-    const char* e = std::getenv("KO_WALK_MAPS");
-    return e ? std::atoi(e) : 0;
-  }();
-  if ((int64_t)n_ref * kv->gqa_group * kv->n_q <= KO_MAX_ROWS && (max_ref_cls == 1 || force_walk)) {
-    // Rounds of growing extent.  Round r reads each of its tuples ONCE up to the extent of the
-    // r-th variant, scores every referenced op at every variant so far (FLOPs, not bytes), and
-    // walks the plan per tuple as far as those margins allow; a tuple that reaches a stage whose
-    // variant is larger is queued for that variant's round.  Nested prefixes ⇒ each round's read
-    // serves all smaller variants.
-    KO_CUDA(cudaMemsetAsync(ws.round_len, 0, sizeof(unsigned long long) * KO_MAX_VARIANTS, s));
-    for (int r = 0; r < n_pv; ++r) {
-      int CPR0 = 1, CPR1 = 0;
-      ko::ScoreParams sp;
-      ko::PrepParams pp;
-      fill_common(sp, pp, kv, ops, ref_ops, n_ref, variants, pv, r + 1, n_ops, n_variants, ws,
-                  &CPR0, &CPR1);
-      if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
-      for (int k = 0; k < n_pv; ++k) {
-        sp.var_round[pv[k]] = k;
-        sp.wl[k] = ws.round_wl + (size_t)k * std::max<int64_t>(kv->n_tuples, 1);
-        sp.wl_len[k] = ws.round_len + k;
-      }
-      if (r == 0) {
-        sp.work = tuple_idx;
-        sp.work_len_host = n_work;
-        sp.work_len_dev = nullptr;
-      } else {
-        sp.work = sp.wl[r];
-        sp.work_len_host = 0;
-        sp.work_len_dev = (const int64_t*)sp.wl_len[r];
-      }
-      sp.round = r;
-      sp.margins = margins;
-      sp.classes = classes;
-      sp.mode = ko::MODE_WALK;
-      sp.n_plans = 1;
-      sp.plans[0] = P;
-      sp.tuple_state = ws.tuple_state;
-      sp.counts = (unsigned long long*)counts;
-      KO_CUDA(ko::launch_prep(pp, s));
-      KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
-      KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
-      if (g_trace_begin && r == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-      KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, n_work * sp.n_l * kv->n_kv_heads, s));
-      if (g_trace_end && r + 1 == n_pv) KO_CUDA(cudaEventRecord(g_trace_end, s));
-    }
-    KO_CUDA(ko::launch_final_counts(rp, s));
-    return KO_OK;
-  }
+  int var_rank[KO_MAX_VARIANTS];
+  for (int v = 0; v < KO_MAX_VARIANTS; ++v) var_rank[v] = 0;
+  for (int k = 0; k < n_pv; ++k) var_rank[pv[k]] = k;
 
-  // fallback: the plan's ops do not fit one 16-row tile — one launch per stage
-  KO_CUDA(ko::launch_route_init(ws.tuple_state, kv->n_tuples, s));
-  for (int s_i = 0; s_i < P.n_stages; ++s_i) {
-    const ko_stage& stg = P.stage[s_i];
-    rp.stage = s_i;
-    KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));  // unit counter + worklist length
-    KO_CUDA(ko::launch_route_reach(rp, s));
-    int op_sel[1] = {stg.op}, var_sel[1] = {stg.variant};
+  // One launch per plan position (= stage): tuples are queued by their own plan walk to the
+  // first later position that computes what they need, so one pass in plan order suffices.
+  KO_CUDA(cudaMemsetAsync(ws.round_len, 0, sizeof(unsigned long long) * KO_MAX_STAGES, s));
+  for (int pos = 0; pos < P.n_stages; ++pos) {
+    const int g = group_of_op[P.stage[pos].op];
+    const int r = var_rank[P.stage[pos].variant];
     int CPR0 = 1, CPR1 = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
-    fill_common(sp, pp, kv, ops, op_sel, 1, variants, var_sel, 1, n_ops, n_variants, ws, &CPR0,
-                &CPR1);
+    fill_common(sp, pp, kv, ops, group_ops[g], group_n[g], variants, pv, r + 1, n_ops, n_variants,
+                ws, &CPR0, &CPR1);
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
-    sp.work = ws.worklist;
-    sp.work_len_host = 0;
-    sp.work_len_dev = (const int64_t*)ws.worklist_len;
+    sp.pos = pos;
+    sp.n_pos = P.n_stages;
+    sp.group = g;
+    sp.round = r;
+    for (int q = 0; q < P.n_stages; ++q) {
+      sp.pos_group[q] = group_of_op[P.stage[q].op];
+      sp.pos_round[q] = var_rank[P.stage[q].variant];
+      sp.wl[q] = ws.round_wl + (size_t)q * std::max<int64_t>(kv->n_tuples, 1);
+      sp.wl_len[q] = ws.round_len + q;
+    }
+    for (int o = 0; o < KO_MAX_OPS; ++o) sp.group_of_op[o] = group_of_op[o];
+    for (int v = 0; v < KO_MAX_VARIANTS; ++v) sp.var_rank[v] = var_rank[v];
+    if (pos == 0) {
+      sp.work = tuple_idx;
+      sp.work_len_host = n_work;
+      sp.work_len_dev = nullptr;
+    } else {
+      sp.work = sp.wl[pos];
+      sp.work_len_host = 0;
+      sp.work_len_dev = (const int64_t*)sp.wl_len[pos];
+    }
     sp.margins = margins;
     sp.classes = classes;
-    sp.mode = ko::MODE_STAGE;
+    sp.mode = ko::MODE_WALK;
     sp.n_plans = 1;
     sp.plans[0] = P;
-    sp.stage_idx = s_i;
     sp.tuple_state = ws.tuple_state;
+    sp.tuple_done = ws.tuple_done;
+    sp.wm = ws.wm;
+    sp.wc = ws.wc;
     sp.counts = (unsigned long long*)counts;
     KO_CUDA(ko::launch_prep(pp, s));
+    KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
-    if (g_trace_begin && s_i == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
+    if (g_trace_begin && pos == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
     KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, n_work * sp.n_l * kv->n_kv_heads, s));
-    if (g_trace_end && s_i + 1 == P.n_stages) KO_CUDA(cudaEventRecord(g_trace_end, s));
+    if (g_trace_end && pos + 1 == P.n_stages) KO_CUDA(cudaEventRecord(g_trace_end, s));
   }
   KO_CUDA(ko::launch_final_counts(rp, s));
   return KO_OK;

@@ -70,12 +70,17 @@ struct ScoreParams {
   // stage mode: apply plan stage `stage_idx` of `plan` (routed execution)
   int32_t stage_idx;
   uint32_t* tuple_state;
-  // walk mode (routed execution by rounds of nested extents): plan walk per tuple
-  int32_t round;
-  int32_t var_local[kMaxVar];  // caller's variant → local index in this launch, -1 = later round
-  int32_t var_round[kMaxVar];  // caller's variant → round that first computes it
-  int32_t* wl[kMaxVar];                 // per-round worklists
-  unsigned long long* wl_len[kMaxVar];  // their lengths (device)
+  // walk mode (routed execution): launch = plan position pos = (operator group, variant rank)
+  int32_t pos, n_pos, group, round;
+  int32_t pos_group[KO_MAX_STAGES], pos_round[KO_MAX_STAGES];
+  int32_t group_of_op[kMaxOps];  // caller's op → group
+  int32_t var_rank[kMaxVar];     // caller's variant → rank (launches of rank r compute ranks ≤ r)
+  int32_t var_local[kMaxVar];    // caller's variant → local index in this launch (-1: absent)
+  int32_t* wl[KO_MAX_STAGES];                 // per-position worklists
+  unsigned long long* wl_len[KO_MAX_STAGES];  // their lengths (device)
+  uint32_t* tuple_done;          // per tuple: 4-bit (rank + 1) computed per group, 15 = none
+  float* wm;                     // computed margins [n_ops][n_variants][n_tuples]
+  int32_t* wc;                   // computed classes
   ko_plan plans[kMaxPlans];
 };
 

@@ -532,10 +532,13 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
           if (c != cls && zz[c] > second) second = zz[c];
         m = zz[cls] - second;
       }
-      if (!walk) {  // walk mode writes only the entries the plan reaches
-        const size_t oi = ((size_t)p.op_ids[o] * p.n_var_total + p.var_ids[v]) * p.n_tuples + t;
+      const size_t oi = ((size_t)p.op_ids[o] * p.n_var_total + p.var_ids[v]) * p.n_tuples + t;
+      if (!walk) {
         if (p.margins) p.margins[oi] = m;
         if (p.classes) p.classes[oi] = cls;
+      } else {  // walk mode: computed margins go to the workspace; only reached ones are output
+        p.wm[oi] = m;
+        p.wc[oi] = cls;
       }
       s_m[warp][p.op_ids[o] * p.n_var + v] = m;  // indexed by the caller's op, local variant
       s_c[warp][p.op_ids[o] * p.n_var + v] = cls;
@@ -545,65 +548,66 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       for (int gp = lane; gp < p.n_plans; gp += 32)
         eval_plan(p.plans[gp], s_m[warp], s_c[warp], p.n_var, p.op_classes_g, p.gold, p.n_tuples,
                   t, s_cnt + gp * kCountsPerPlan);
-    } else if (walk) {
-      if (lane == 0) {
-        // routed execution: walk the plan from where the tuple stopped, deciding every stage
-        // whose variant this round computed (Eqs. accept-i/reject-i/unsure-i)
-        const ko_plan& P = p.plans[0];
-        uint32_t state = p.round == 0 ? 1u : p.tuple_state[t];
-        int s = (int)((state >> 24) & 15u);
-        for (; s < P.n_stages; ++s) {
-          const ko_stage& st = P.stage[s];
-          const int o = st.op;
-          if (!(state & 1u) || op_status(state, o) != 0) continue;  // not reached
-          const int vl = p.var_local[st.variant];
-          if (vl < 0) {  // its variant's extent comes in a later round
-            const int r = p.var_round[st.variant];
-            const unsigned long long pos = atomicAdd(p.wl_len[r], 1ull);
-            p.wl[r][pos] = (int32_t)t;
-            break;
+    } else if (walk && lane == 0) {
+      // Routed execution: this launch is plan position `pos` = (operator group, variant rank).
+      // Walk the plan from where the tuple stopped, deciding every reached stage whose margin
+      // is available (its group was computed for this tuple at a rank ≥ the stage variant's);
+      // stop at the first one that is not and queue the tuple for the next position that
+      // computes it (Eqs. accept-i/reject-i/unsure-i; inter-op reach P:536-539).
+      const ko_plan& P = p.plans[0];
+      uint32_t state = p.pos == 0 ? 1u : p.tuple_state[t];
+      uint32_t done = p.pos == 0 ? 0xFFFFFFFFu : p.tuple_done[t];  // 4-bit rank+1 per group
+      {
+        const uint32_t cur = (done >> (4 * p.group)) & 15u;
+        const uint32_t mine = (uint32_t)p.round + 1u;
+        if (cur == 15u || cur < mine) done = (done & ~(15u << (4 * p.group))) | (mine << (4 * p.group));
+      }
+      int s = (int)((state >> 24) & 15u);
+      for (; s < P.n_stages; ++s) {
+        const ko_stage& st = P.stage[s];
+        const int o = st.op;
+        if (!(state & 1u) || op_status(state, o) != 0) continue;  // not reached
+        const int g = p.group_of_op[o];
+        const int rk = p.var_rank[st.variant];
+        const uint32_t have = (done >> (4 * g)) & 15u;      // 15: never computed
+        if (have == 15u || (int)have - 1 < rk) {
+          // the next position computing (g, ≥ rk) exists: stage s itself is one (s > pos)
+          int q = p.pos + 1;
+          while (q < p.n_pos && !(p.pos_group[q] == g && p.pos_round[q] >= rk)) ++q;
+          if (q < p.n_pos) {
+            const unsigned long long at = atomicAdd(p.wl_len[q], 1ull);
+            p.wl[q][at] = (int32_t)t;
           }
-          const float m = s_m[warp][o * p.n_var + vl];
-          const int32_t cls = s_c[warp][o * p.n_var + vl];
-          const size_t oi = ((size_t)o * p.n_var_total + st.variant) * p.n_tuples + t;
-          if (p.margins) p.margins[oi] = m;
-          if (p.classes) p.classes[oi] = cls;
-          int* cnt = s_cnt + 5 + 4 * s;
-          atomicAdd(&cnt[0], 1);
-          const int d = decide(m, st, p.op_classes_g[o]);
-          if (d == D_ACCEPT || d == D_RESOLVED) {
-            state |= 1u << (1 + 2 * o);
-            if (d == D_RESOLVED) state |= ((uint32_t)cls & 15u) << (16 + 4 * o);
-            atomicAdd(&cnt[1], 1);
-          } else if (d == D_REJECT) {
-            state = (state & ~1u) | (2u << (1 + 2 * o));
-            atomicAdd(&cnt[2], 1);
-          } else {
-            atomicAdd(&cnt[3], 1);
-          }
+          break;
         }
-        p.tuple_state[t] = (state & ~(15u << 24)) | ((uint32_t)s << 24);
+        const size_t oi = ((size_t)o * p.n_var_total + st.variant) * p.n_tuples + t;
+        float m;
+        int32_t cls;
+        if (g == p.group) {
+          m = s_m[warp][o * p.n_var + p.var_local[st.variant]];
+          cls = s_c[warp][o * p.n_var + p.var_local[st.variant]];
+        } else {
+          m = __ldcg(p.wm + oi);
+          cls = __ldcg(p.wc + oi);
+        }
+        if (p.margins) p.margins[oi] = m;
+        if (p.classes) p.classes[oi] = cls;
+        int* cnt = s_cnt + 5 + 4 * s;
+        atomicAdd(&cnt[0], 1);
+        const int d = decide(m, st, p.op_classes_g[o]);
+        if (d == D_ACCEPT || d == D_RESOLVED) {
+          state |= 1u << (1 + 2 * o);
+          if (d == D_RESOLVED) state |= ((uint32_t)cls & 15u) << (16 + 4 * o);
+          atomicAdd(&cnt[1], 1);
+        } else if (d == D_REJECT) {
+          state = (state & ~1u) | (2u << (1 + 2 * o));
+          atomicAdd(&cnt[2], 1);
+        } else {
+          atomicAdd(&cnt[3], 1);
+        }
       }
-    } else if (lane == 0 && p.tuple_state) {
-      // routed execution, one stage per launch (fallback when the plan's ops do not fit one
-      // row tile): apply stage `stage_idx` (this launch has exactly its op and variant)
-      const ko_stage& st = p.plans[0].stage[p.stage_idx];
-      const int o = st.op;
-      const int d = decide(s_m[warp][o * p.n_var + 0], st, p.op_classes[0]);
-      uint32_t state = p.tuple_state[t];
-      int* cnt = s_cnt + 5 + 4 * p.stage_idx;
-      atomicAdd(&cnt[0], 1);
-      if (d == D_ACCEPT || d == D_RESOLVED) {
-        state |= 1u << (1 + 2 * o);
-        if (d == D_RESOLVED) state |= ((uint32_t)s_c[warp][o * p.n_var + 0] & 15u) << (16 + 4 * o);
-        atomicAdd(&cnt[1], 1);
-      } else if (d == D_REJECT) {
-        state = (state & ~1u) | (2u << (1 + 2 * o));
-        atomicAdd(&cnt[2], 1);
-      } else {
-        atomicAdd(&cnt[3], 1);
-      }
-      p.tuple_state[t] = state;
+      p.tuple_state[t] = (state & ~(15u << 24)) | ((uint32_t)s << 24);
+      p.tuple_done[t] = done;
     }
     }  // last
   }
