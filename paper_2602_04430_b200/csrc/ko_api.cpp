@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -272,6 +273,25 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   sp.done = ws.done;
   sp.unit_counter = ws.unit_counter;
   sp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kv->head_dim));
+  // Work-unit size: a unit streams HG kv-heads of one (tuple, layer) back-to-back, HG chosen so
+  // a unit is ~32 pages (estimated from the pool's average pages per tuple and the largest
+  // keep‰), which hides the per-unit start-up latency behind the stream for short tuples.
+  {
+    int max_keep = 1;
+    for (int i = 0; i < n_vsel; ++i) max_keep = std::max(max_keep, (int)variants[var_sel[i]].keep_permille);
+    const double ppu = kv->n_tuples > 0
+                           ? (double)kv->n_pages / (double)kv->n_tuples * max_keep / 1000.0
+                           : 32.0;
+    static const int hg_env = [] {  // tuning knob for A/B measurements
+      const char* e = std::getenv("KO_HEADS_PER_UNIT");
+      return e ? std::atoi(e) : 0;
+    }();
+    int hg = 1;
+    while (hg * 2 <= kv->n_kv_heads && kv->n_kv_heads % (hg * 2) == 0 && (hg * 2) * ppu <= 32.0)
+      hg *= 2;
+    if (hg_env > 0 && kv->n_kv_heads % hg_env == 0) hg = hg_env;
+    sp.heads_per_unit = hg;
+  }
   pp.n_l = n_l;
   pp.n_kv_heads = kv->n_kv_heads;
   pp.gqa = kv->gqa_group;

@@ -62,6 +62,7 @@ struct ScoreParams {
   float* margins;   // [n_ops_total][n_var_total][n_tuples] or NULL
   int32_t* classes;  // same or NULL
   float scale_log2;  // log2(e)/sqrt(head_dim)
+  int32_t heads_per_unit;  // kv-heads one work unit streams back-to-back (divides n_kv_heads)
   // grid mode: per-tuple evaluation of every plan (indices are caller's = local here)
   int32_t mode;
   int32_t n_plans;

@@ -227,7 +227,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 
   const int64_t n_work = p.work_len_dev ? *p.work_len_dev : p.work_len_host;
   const int Hkv = p.n_kv_heads;
-  const int upt = p.n_l * Hkv;  // work units per tuple: one per (layer, kv-head)
+  const int HG = p.heads_per_unit;  // kv-heads streamed back-to-back by one unit (same pages)
+  const int upt = p.n_l * (Hkv / HG);  // work units per tuple: (layer, group of HG kv-heads)
   const int64_t n_units = n_work * upt;
   const int R = p.n_ops * p.rows_per_op;
 
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     if (u >= n_units) break;
     const int64_t wslot = u / upt;
     const int unit = (int)(u - wslot * upt);
-    const int l = unit / Hkv, h = unit - (unit / Hkv) * Hkv;
+    const int l = unit / (Hkv / HG), h0 = (unit - l * (Hkv / HG)) * HG;
     const int64_t t = p.work ? (int64_t)p.work[wslot] : wslot;
     const int L = p.seq_len[t];
 
@@ -261,17 +262,20 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     int n_need = 0;
     for (int v = 0; v < p.n_var; ++v)
       if (p.cut[v] > l) n_need = max(n_need, n_kept(L, p.keep[v]));
-    int next_snap = n_need;  // smallest active n_kept (first snapshot point)
+    int first_snap = n_need;  // smallest active n_kept (first snapshot point)
     for (int v = 0; v < p.n_var; ++v)
-      if (p.cut[v] > l) next_snap = min(next_snap, n_kept(L, p.keep[v]));
+      if (p.cut[v] > l) first_snap = min(first_snap, n_kept(L, p.keep[v]));
 
     const int64_t pbase = p.page_indptr[t];
     const int n_pages = (n_need + 15) >> 4;
     int pid_chunk = 0;
     int pid_reg = lane < n_pages ? __ldg(p.page_ids + pbase + lane) : 0;
 
-    // TMA issue of page `pg` of this unit into the next ring slot (whole warp calls; lane 0 acts)
-    auto issue = [&](int pg) {
+    // TMA issue of stream page k = hh·n_pages + pg of this unit (head h0 + hh) into the next
+    // ring slot (whole warp calls; lane 0 issues)
+    auto issue = [&](int k) {
+      const int hh = k / n_pages, pg = k - hh * n_pages;
+      const int h = h0 + hh;
       const int chunk = pg >> 5;
       if (chunk != pid_chunk) {
         const int idx = (chunk << 5) + lane;
@@ -291,8 +295,14 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       ++issued;
     };
     // prologue: fill the ring (all earlier stages have been consumed)
-    const int n_pro = min(S, n_pages);
+    const int n_stream = HG * n_pages;
+    const int n_pro = min(S, n_stream);
     for (int k = 0; k < n_pro; ++k) issue(k);
+
+   for (int hh = 0; hh < HG; ++hh) {
+    const int h = h0 + hh;
+    const int unit_lh = l * Hkv + h;  // partial-logit slot of (layer, kv-head)
+    int next_snap = first_snap;
 
     // operator-query fragments for (l, h)
     const int lh = l * Hkv + h;
@@ -377,9 +387,9 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       // the stage's bytes are in registers: hand the slot back to TMA for page pg + S
       __syncwarp();
       ++consumed;
-      if (pg + S < n_pages) {
+      if (hh * n_pages + pg + S < n_stream) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(pg + S);
+        issue(hh * n_pages + pg + S);
       }
       // ---- per-lane token indices and values: k = nt*2 + e ↔ token pg*16 + nt*8 + 2q + e
       const int page_hi = min(pg * 16 + 16, n_need);
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 #pragma unroll
               for (int o = 0; o < kMaxOps; ++o) {
                 if (o >= p.n_ops) break;
-                float* dst = p.part + ((((size_t)wslot * upt + unit) * p.n_ops + o) * p.n_var + v) * CPR;
+                float* dst = p.part + ((((size_t)wslot * p.n_l * Hkv + unit_lh) * p.n_ops + o) * p.n_var + v) * CPR;
 #pragma unroll
                 for (int c = 0; c < CPR; ++c) dst[c] = opv[o][c];
               }
@@ -482,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       }
     }
 
+   }  // heads of the unit
     // ---- tuple completion: the warp finishing the tuple's last unit finalises it
     __syncwarp();
     int last = 0;
@@ -507,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       float zf = -CUDART_INF_F;
       if (c < p.op_classes[o]) {
         double z = (double)__ldg(p.bias[o] + c);
-        const float* src = p.part + ((size_t)wslot * upt * p.n_ops + o) * p.n_var * CPR + v * CPR + c;
+        const float* src = p.part + ((size_t)wslot * p.n_l * Hkv * p.n_ops + o) * p.n_var * CPR + v * CPR + c;
         const size_t ustride = (size_t)p.n_ops * p.n_var * CPR;
         const int u_end = min(p.cut[v], p.n_l) * Hkv;  // units are l-major: l < cut ⇔ u < cut·Hkv
         for (int uu = 0; uu < u_end; ++uu) z += (double)__ldcg(src + uu * ustride);
