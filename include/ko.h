@@ -100,8 +100,11 @@ typedef struct {
 typedef struct {
   int32_t n_classes; /* 1 = filter (z_0 = yes−no log-odds), 2..KO_MAX_CLASSES = map-classify */
   const void* q;     /* bf16 [n_layers][n_kv_heads*gqa_group][n_q][head_dim], post-RoPE       */
-  const float* w;    /* fp32 [n_classes][n_layers][n_kv_heads*gqa_group][n_q][head_dim]       */
+  const void* w;     /* readout [n_classes][n_layers][n_kv_heads*gqa_group][n_q][head_dim]:
+                        fp32 (entered as bf16 hi + lo, error ≤ 2^-17 |w|) or, with w_is_bf16,
+                        bf16 (exact; a K-class map then needs half the tensor-core tiles)      */
   const float* b;    /* fp32 [n_classes]                                                      */
+  int32_t w_is_bf16; /* 0: w is fp32; 1: w is bf16                                            */
 } ko_operator;
 
 typedef struct {

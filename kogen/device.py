@@ -11,7 +11,7 @@ from .workloads import Workload, gold_from_labels
 
 
 def device_workload(wl: Workload, t0: int = 0, n: Optional[int] = None, device: str = "cuda",
-                    placement: str = "affine", poison: bool = True):
+                    placement: str = "affine", poison: bool = True, w_dtype: str = "bf16"):
     """Returns dict(kv, ops, gold, seq_len, indptr, page_ids) for tuples t0 .. t0+n-1.
 
     kv.pool is generated on the device (bit-identical to kogen.host_pool); gold is the latent
@@ -35,19 +35,27 @@ def device_workload(wl: Workload, t0: int = 0, n: Optional[int] = None, device: 
                     seq_len=torch.from_numpy(seq_len).to(device), n_layers=spec.n_layers,
                     n_kv_heads=spec.n_kv_heads, gqa_group=spec.gqa, head_dim=spec.head_dim,
                     n_q=spec.n_q)
-    ops = host_ops_to_device(wl, device)
+    ops = host_ops_to_device(wl, device, w_dtype)
     gold = torch.from_numpy(gold_from_labels(spec.labels(t0, n), spec.op_classes)).to(device)
     return dict(kv=kv, ops=ops, gold=gold, seq_len=seq_len, indptr=indptr, page_ids=ids)
 
 
-def host_ops_to_device(wl: Workload, device: str = "cuda"):
+def host_ops_to_device(wl: Workload, device: str = "cuda", w_dtype: str = "bf16"):
+    """Operators on the device.  The generator's readout is exactly representable in bf16
+    (|int| ≤ 138 over a power of two), so w_dtype="bf16" passes the same values."""
     import torch
     import paper_2602_04430_b200 as ko
     bias = wl.biases()
     ops = []
     for o in range(wl.spec.n_ops):
         q = torch.from_numpy(wl.spec.q(o).view(np.int16)).to(device).view(torch.bfloat16)
-        w = torch.from_numpy(wl.spec.w(o)).to(device)
+        w32 = torch.from_numpy(wl.spec.w(o))
+        if w_dtype == "bf16":
+            wb = w32.to(torch.bfloat16)
+            assert torch.equal(wb.float(), w32), "readout not exact in bf16"
+            w = wb.to(device)
+        else:
+            w = w32.to(device)
         b = torch.tensor(bias[o], dtype=torch.float32, device=device)
         ops.append(ko.Operator(wl.spec.op_classes[o], q, w, b))
     return ops

@@ -41,7 +41,7 @@ class _KV(ctypes.Structure):
 
 class _Op(ctypes.Structure):
     _fields_ = [("n_classes", ctypes.c_int32), ("q", ctypes.c_void_p), ("w", ctypes.c_void_p),
-                ("b", ctypes.c_void_p)]
+                ("b", ctypes.c_void_p), ("w_is_bf16", ctypes.c_int32)]
 
 
 class _Variant(ctypes.Structure):
@@ -145,7 +145,7 @@ class Operator:
     """One logical operator (ko_operator): n_classes 1 = filter, >= 2 = map-classify."""
     n_classes: int
     q: "torch.Tensor"   # bf16 [n_layers][Hq][n_q][D]
-    w: "torch.Tensor"   # fp32 [n_classes][n_layers][Hq][n_q][D]
+    w: "torch.Tensor"   # fp32 or bf16 [n_classes][n_layers][Hq][n_q][D]
     b: "torch.Tensor"   # fp32 [n_classes]
 
 
@@ -158,7 +158,11 @@ def _ops(ops: Sequence[Operator]):
         for name in ("q", "w", "b"):
             if not getattr(o, name).is_cuda:
                 raise ValueError(f"Operator.{name} must be a CUDA tensor")
-        arr[i] = _Op(int(o.n_classes), o.q.data_ptr(), o.w.data_ptr(), o.b.data_ptr())
+        import torch
+        w_bf16 = 1 if o.w.dtype == torch.bfloat16 else 0
+        if not w_bf16 and o.w.dtype != torch.float32:
+            raise ValueError("Operator.w must be float32 or bfloat16")
+        arr[i] = _Op(int(o.n_classes), o.q.data_ptr(), o.w.data_ptr(), o.b.data_ptr(), w_bf16)
     return arr
 
 

@@ -256,7 +256,8 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
     sp.op_classes[i] = op.n_classes;
     sp.bias[i] = op.b;
     pp.q[i] = (const uint16_t*)op.q;
-    pp.w[i] = op.w;
+    pp.w[i] = op.w_is_bf16 ? nullptr : (const float*)op.w;
+    pp.w_bf16[i] = op.w_is_bf16 ? (const uint16_t*)op.w : nullptr;
     pp.op_classes[i] = op.n_classes;
     for (int r = 0; r < sp.rows_per_op; ++r, ++slot) {
       sp.slot_op[slot] = i;
@@ -267,6 +268,10 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   }
   *CPR0 = pow2_at_least(std::max(half_cls[0], 1));
   *CPR1 = half_cls[1] ? pow2_at_least(half_cls[1]) : 0;
+  // bf16 readouts of a multi-class tile: two classes per W·V tile (no lo residual)
+  bool all_bf16 = true;
+  for (int i = 0; i < n_sel; ++i) all_bf16 = all_bf16 && ops[op_sel[i]].w_is_bf16;
+  pp.nolo = all_bf16 && *CPR0 >= 2 && *CPR1 == 0;
   sp.qfrag = ws.qfrag;
   sp.wfrag = ws.wfrag;
   sp.part = ws.part;
@@ -384,7 +389,8 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, n_work * sp.n_l * kv->n_kv_heads, s));
+    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0,
+                             n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end) KO_CUDA(cudaEventRecord(g_trace_end, s));
     return KO_OK;
   }
@@ -489,7 +495,8 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin && pos == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, n_work * sp.n_l * kv->n_kv_heads, s));
+    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0,
+                             n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end && pos + 1 == P.n_stages) KO_CUDA(cudaEventRecord(g_trace_end, s));
   }
   KO_CUDA(ko::launch_final_counts(rp, s));

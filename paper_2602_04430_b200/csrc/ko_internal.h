@@ -91,7 +91,9 @@ struct PrepParams {
   int32_t slot_op[16];   // row slot → local op (-1 = padding)
   int32_t slot_rem[16];  // row slot → row within the op (gqa member * n_q + query row)
   const uint16_t* q[kMaxOps];
-  const float* w[kMaxOps];
+  const float* w[kMaxOps];          // fp32 readout, or NULL when w_bf16 is given
+  const uint16_t* w_bf16[kMaxOps];  // bf16 readout (ko_operator.w_is_bf16)
+  int32_t nolo;                     // all ops bf16: two classes per W·V tile, no lo part
   int32_t op_classes[kMaxOps];
   uint4* qfrag;
   uint4* wfrag;
@@ -143,8 +145,8 @@ cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s);
 
 // launchers (ko_kernels.cu); return cudaSuccess or the launch error
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
-cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, int64_t max_units,
-                         cudaStream_t s);
+cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, bool nolo,
+                         int64_t max_units, cudaStream_t s);
 cudaError_t launch_route_reach(const RouteParams& p, cudaStream_t s);  // build worklist for stage
 cudaError_t launch_route_apply(const RouteParams& p, cudaStream_t s);  // apply stage on margins
 cudaError_t launch_route_plan(const RouteParams& p, cudaStream_t s);   // whole plan on margins

@@ -186,15 +186,21 @@ struct Ring {
 };
 
 // CPR0 / CPR1: classes per row slot in half 0 (A rows g) / half 1 (A rows g+8) of the row tile;
-// CPR1 = 0 when at most 8 rows attend a kv-head.  W·V tiles: CPR0 + CPR1 (half h, class c →
-// tile h ? CPR0 + c : c); partial logits are stored with stride CPR = CPR0 (≥ every op's classes).
-template <int D, int CPR0, int CPR1>
+// CPR1 = 0 when at most 8 rows attend a kv-head; partial logits are stored with stride
+// CPR = CPR0 (≥ every op's classes).  W·V tiles:
+//   fp32 W (NOLO = false): bf16 hi in A rows 0-7 + lo in rows 8-15 of one tile per (half, class):
+//     tile(h, c) = h ? CPR0 + c : c, u = C[e] + C[2+e];
+//   bf16 W (NOLO = true, exact: no lo part): two classes per tile, class c in rows 0-7 (c even)
+//     or 8-15 (c odd): tile(h, c) = (h ? ⌈CPR0/2⌉ : 0) + c/2, u = C[2(c&1) + e].
+template <int D, int CPR0, int CPR1, bool NOLO>
 __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_constant__ ScoreParams p) {
   constexpr int KS = D / 16;  // mma k-steps over head_dim
   constexpr int KP = D / 32;  // 128-bit fragment reads per token row per lane (2 k-steps each)
   constexpr int NH = CPR1 > 0 ? 2 : 1;
   constexpr int CPR = CPR0;
-  constexpr int NT = CPR0 + CPR1;
+  constexpr int T0 = NOLO ? (CPR0 + 1) / 2 : CPR0;  // tiles of half 0
+  constexpr int NT = NOLO ? T0 + (CPR1 + 1) / 2 : CPR0 + CPR1;
+  constexpr int WREG = NT <= 2 ? NT : 0;            // W·V tiles whose fragments stay in registers
   constexpr int S = Ring<D>::kStages;
   constexpr int STAGE = Ring<D>::kStageBytes;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -312,14 +318,14 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       const uint4 f = __ldg(p.qfrag + ((size_t)lh * KS + ks) * 32 + lane);
       qa[ks][0] = f.x; qa[ks][1] = f.y; qa[ks][2] = f.z; qa[ks][3] = f.w;
     }
-    uint32_t wa1[NT == 1 ? KS : 1][4];
-    if constexpr (NT == 1) {
+    uint32_t wa1[WREG > 0 ? WREG : 1][KS][4];
+#pragma unroll
+    for (int tt = 0; tt < WREG; ++tt)
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
-        const uint4 f = __ldg(p.wfrag + ((size_t)lh * KS + ks) * 32 + lane);
-        wa1[ks][0] = f.x; wa1[ks][1] = f.y; wa1[ks][2] = f.z; wa1[ks][3] = f.w;
+        const uint4 f = __ldg(p.wfrag + (((size_t)lh * NT + tt) * KS + ks) * 32 + lane);
+        wa1[tt][ks][0] = f.x; wa1[tt][ks][1] = f.y; wa1[tt][ks][2] = f.z; wa1[tt][ks][3] = f.w;
       }
-    }
     const uint4* wbase = p.wfrag + (size_t)lh * NT * KS * 32 + lane;
 
     // lane-local online-softmax state per half-slot (log2 domain)
@@ -370,9 +376,12 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 #pragma unroll
           for (int j = 0; j < KP; ++j) {
             uint32_t a0[4], a1[4];
-            if constexpr (NT == 1) {
+            if constexpr (WREG > 0) {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) { a0[i] = wa1[2 * j][i]; a1[i] = wa1[2 * j + 1][i]; }
+              for (int i = 0; i < 4; ++i) {
+                a0[i] = wa1[tt][2 * j][i];
+                a1[i] = wa1[tt][2 * j + 1][i];
+              }
             } else {
               const uint4 f0 = __ldg(wbase + ((size_t)tt * KS + 2 * j) * 32);
               const uint4 f1 = __ldg(wbase + ((size_t)tt * KS + 2 * j + 1) * 32);
@@ -417,12 +426,13 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
             sm[hs] = sm[hs] * corr + ((ps[0] + ps[1]) + (ps[2] + ps[3]));
 #pragma unroll
             for (int c = 0; c < (hs == 0 ? CPR0 : CPR1); ++c) {
-              const int tt = hs == 0 ? c : CPR0 + c;
+              const int tt = NOLO ? (hs == 0 ? 0 : T0) + c / 2 : (hs == 0 ? c : CPR0 + c);
               float a = ac[hs][c] * corr;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const int nt = k >> 1, e = k & 1;
-                a = fmaf(ps[k], U[tt][nt][e] + U[tt][nt][2 + e], a);
+                const float u = NOLO ? U[tt][nt][2 * (c & 1) + e] : U[tt][nt][e] + U[tt][nt][2 + e];
+                a = fmaf(ps[k], u, a);
               }
               ac[hs][c] = a;
             }
@@ -639,7 +649,7 @@ __device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) {
 
 __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
   const int KS = p.head_dim / 16;
-  const int NT = p.CPR0 + p.CPR1;
+  const int NT = p.nolo ? (p.CPR0 + 1) / 2 + (p.CPR1 + 1) / 2 : p.CPR0 + p.CPR1;
   const int Hq = p.n_kv_heads * p.gqa;
   const int n_lh = p.n_l * p.n_kv_heads;
   const int64_t nq_items = (int64_t)n_lh * KS * 32;
@@ -672,20 +682,42 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
         }
       }
     } else {
-      const int hs = tt < p.CPR0 ? 0 : 1, c = tt < p.CPR0 ? tt : tt - p.CPR0;
-      const int rho = hs * 8 + g;
-      for (int k = 0; k < 4; ++k) {
-        float w = 0.f;
-        if (p.slot_op[rho] >= 0) {
-          const int o = p.slot_op[rho], rem = p.slot_rem[rho];
-          const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
-          if (c < p.op_classes[o])
-            w = p.w[o][((((size_t)c * p.n_layers + l) * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k];
+      if (!p.nolo) {
+        // fp32 W: tile (half, class) holds bf16 hi in A rows 0-7 and the lo residual in 8-15
+        const int hs = tt < p.CPR0 ? 0 : 1, c = tt < p.CPR0 ? tt : tt - p.CPR0;
+        const int rho = hs * 8 + g;
+        for (int k = 0; k < 4; ++k) {
+          float w = 0.f;
+          if (p.slot_op[rho] >= 0) {
+            const int o = p.slot_op[rho], rem = p.slot_rem[rho];
+            const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
+            if (c < p.op_classes[o]) {
+              const size_t wi = ((((size_t)c * p.n_layers + l) * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k;
+              w = p.w_bf16[o] ? __bfloat162float(__ushort_as_bfloat16(p.w_bf16[o][wi])) : p.w[o][wi];
+            }
+          }
+          const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+          const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
+          vals[0][k] = __bfloat16_as_ushort(hi);  // A rows 0-7: W_hi
+          vals[1][k] = __bfloat16_as_ushort(lo);  // A rows 8-15: W_lo
         }
-        const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-        const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
-        vals[0][k] = __bfloat16_as_ushort(hi);  // A rows 0-7: W_hi
-        vals[1][k] = __bfloat16_as_ushort(lo);  // A rows 8-15: W_lo
+      } else {
+        // bf16 W (exact): tile = (half, class pair); class 2τ' in A rows 0-7, 2τ'+1 in 8-15
+        const int T0 = (p.CPR0 + 1) / 2;
+        const int hs = tt < T0 ? 0 : 1, c0 = 2 * (tt < T0 ? tt : tt - T0);
+        const int rho = hs * 8 + g;
+        for (int hr = 0; hr < 2; ++hr)
+          for (int k = 0; k < 4; ++k) {
+            uint16_t b = 0;
+            const int c = c0 + hr;
+            if (p.slot_op[rho] >= 0) {
+              const int o = p.slot_op[rho], rem = p.slot_rem[rho];
+              const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
+              if (c < p.op_classes[o])
+                b = p.w_bf16[o][((((size_t)c * p.n_layers + l) * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k];
+            }
+            vals[hr][k] = b;
+          }
       }
     }
     uint4 out;
@@ -871,14 +903,14 @@ int num_sms() {
   return n;
 }
 
-template <int D, int CPR0, int CPR1>
+template <int D, int CPR0, int CPR1, bool NOLO>
 cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t s) {
   static int occ = 0;
   constexpr int smem = Ring<D>::kSmemBytes;
   if (!occ) {
-    cudaFuncSetAttribute(ko_score_kernel<D, CPR0, CPR1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(ko_score_kernel<D, CPR0, CPR1, NOLO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ko_score_kernel<D, CPR0, CPR1>, kThreads,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ko_score_kernel<D, CPR0, CPR1, NOLO>, kThreads,
                                                   smem);
     if (occ < 1) occ = 1;
   }
@@ -887,7 +919,7 @@ cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t
   const int64_t need = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  ko_score_kernel<D, CPR0, CPR1><<<(unsigned)grid, kThreads, smem, s>>>(p);
+  ko_score_kernel<D, CPR0, CPR1, NOLO><<<(unsigned)grid, kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -898,18 +930,24 @@ cudaError_t launch_prep(const PrepParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, int64_t max_units,
-                         cudaStream_t s) {
-#define KO_DISPATCH(DD, C0, C1) \
-  if (head_dim == DD && CPR0 == C0 && CPR1 == C1) return launch_score_t<DD, C0, C1>(p, max_units, s);
+cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, bool nolo,
+                         int64_t max_units, cudaStream_t s) {
+#define KO_DISPATCH(DD, C0, C1)                                                       \
+  if (head_dim == DD && CPR0 == C0 && CPR1 == C1 && !nolo)                           \
+    return launch_score_t<DD, C0, C1, false>(p, max_units, s);
+#define KO_DISPATCH_NOLO(DD, C0)                                                      \
+  if (head_dim == DD && CPR0 == C0 && CPR1 == 0 && nolo)                             \
+    return launch_score_t<DD, C0, 0, true>(p, max_units, s);
 #define KO_DISPATCH_D(DD)                                                                  \
   KO_DISPATCH(DD, 1, 0) KO_DISPATCH(DD, 1, 1) KO_DISPATCH(DD, 2, 0) KO_DISPATCH(DD, 2, 1)   \
   KO_DISPATCH(DD, 2, 2) KO_DISPATCH(DD, 4, 0) KO_DISPATCH(DD, 4, 1) KO_DISPATCH(DD, 4, 2)   \
   KO_DISPATCH(DD, 4, 4) KO_DISPATCH(DD, 8, 0) KO_DISPATCH(DD, 8, 1) KO_DISPATCH(DD, 8, 2)   \
-  KO_DISPATCH(DD, 8, 4) KO_DISPATCH(DD, 8, 8)
+  KO_DISPATCH(DD, 8, 4) KO_DISPATCH(DD, 8, 8)                                              \
+  KO_DISPATCH_NOLO(DD, 2) KO_DISPATCH_NOLO(DD, 4) KO_DISPATCH_NOLO(DD, 8)
   KO_DISPATCH_D(64)
   KO_DISPATCH_D(128)
 #undef KO_DISPATCH_D
+#undef KO_DISPATCH_NOLO
 #undef KO_DISPATCH
   return cudaErrorInvalidValue;
 }

@@ -32,7 +32,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(ko._Stage) == 20
     assert ctypes.sizeof(ko._Plan) == 4 + 8 * 20
     assert ctypes.sizeof(ko._KV) == 5 * 4 + 4 + 8 * 6   # 5 ints, pad, pointer/int64 fields
-    assert ctypes.sizeof(ko._Op) == 32
+    assert ctypes.sizeof(ko._Op) == 40
 
 
 def _kv(head_dim=128, layers=2, gqa=4):
@@ -46,7 +46,7 @@ def _ops(n=1, classes=1):
     fake = 1 << 20
     arr = (ko._Op * n)()
     for i in range(n):
-        arr[i] = ko._Op(classes, fake, fake, fake)
+        arr[i] = ko._Op(classes, fake, fake, fake, 0)
     return arr
 
 

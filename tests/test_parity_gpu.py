@@ -37,16 +37,24 @@ CASES = [
     ("d64_rows12_maps", Geom(2, 1, 4, 64, 1), [3, 40, 77], (1, 3, 1), [(1000, 2), (600, 2), (250, 1)]),
     ("d128_nq2_rows16", Geom(1, 2, 4, 128, 2), [9, 63, 64, 65], (1, 2), [(1000, 1), (777, 1)]),
     ("d64_c8", Geom(1, 1, 2, 64, 1), [20, 50], (8,), [(1000, 1)]),
+    ("d128_map3_g2", Geom(2, 2, 2, 128, 2), [7, 40, 100], (3,), [(1000, 2), (500, 1)]),
 ]
 
 
+@pytest.mark.parametrize("w_bf16", [False, True], ids=["w_fp32", "w_bf16"])
 @pytest.mark.parametrize("name,geom,lengths,classes,variants", CASES, ids=[c[0] for c in CASES])
-def test_score_parity_random(ko, name, geom, lengths, classes, variants):
+def test_score_parity_random(ko, name, geom, lengths, classes, variants, w_bf16):
+    """fp32 readouts (bf16 hi + lo tiles) and bf16 readouts (two classes per tile for maps)."""
     rng = np.random.default_rng(abs(hash(name)) % 2**32)
     K, V, ops_h = random_problem(rng, geom, lengths, n_ops=len(classes), classes=classes)
     pool, indptr, ids, sl = build_pool(K, V, lengths, poison=True)
     m_or, c_or = run_oracle_on_host(pool, indptr, ids, sl, geom, ops_h, variants)
     kv, ops = tensors_to_device(pool, indptr, ids, sl, geom, ops_h)
+    if w_bf16:                                       # the random readouts are exact in bf16
+        for op in ops:
+            wb = op.w.to(torch.bfloat16)
+            assert torch.equal(wb.float(), op.w)
+            op.w = wb
     m, c, _ = ko.score_batch(kv, ops, variants)
     torch.cuda.synchronize()
     err = parity.assert_margins(m.cpu().numpy(), m_or)
