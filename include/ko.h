@@ -111,6 +111,9 @@ typedef struct {
   int32_t keep_permille; /* 1..1000: n_kept = max(1, floor(L·keep/1000)) (Q3)             */
   int32_t layer_cut;     /* 1..n_layers: layers l < layer_cut are consulted              */
 } ko_variant;
+/* A variant with keep_permille == 0 and layer_cut == 0 is EXTERNAL: its margins are supplied
+ * by the caller in the margins array (e.g. an embedding-similarity stage, ko_embed_scores) and
+ * plans may use it like any other (filters only).  ko_score_batch never overwrites them.      */
 
 typedef struct {
   int32_t op, variant; /* indices into the call's ops[] and variants[]                   */
@@ -180,6 +183,18 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
                           const int32_t* classes, const int32_t* n_classes, int32_t n_ops,
                           int32_t n_variants, int64_t n_tuples, const uint8_t* gold,
                           int64_t* counts, void* stream);
+
+/* ko_embed_scores — the embedding-similarity filter stage ("a lightweight embedding-based
+ * operator that computes similarities between data and query embeddings and applies a decision
+ * threshold", P:456-458 two thresholds, Blip P:746; NEXT-3): for every tuple t (tuple_idx or all)
+ * and every operator embedding e, margins[op_ids[e]][variant][t] = cos(item_emb[t], op_emb[e]).
+ * item_emb: device bf16 [n_tuples][dim] (16-byte aligned); op_emb: device bf16 [n_emb][dim];
+ * op_ids: host int32 [n_emb]; dim a multiple of 8 (≤ 4096); fp32 accumulation.  Use a variant
+ * marked external (keep‰ = layer_cut = 0) to chain it into plans.                              */
+ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, const void* op_emb,
+                          int32_t n_emb, const int32_t* op_ids, int32_t n_ops, int32_t variant,
+                          int32_t n_variants, const int32_t* tuple_idx, int64_t n_idx,
+                          float* margins, void* stream);
 
 /* ko_soft_stats — the continuous relaxation of one plan (NEXT-1 of SURVEY §8(f)) on
  * precomputed margins: pick factors σ_i = sigmoid(s_i/τ) (final stages σ = 1), soft decisions

@@ -56,6 +56,8 @@ def lib():
         L.kg_fill_w.argtypes = [ctypes.POINTER(KgCfg), ctypes.c_int32, P]
         L.kg_fill_meta.argtypes = [ctypes.POINTER(KgCfg), ctypes.c_int64, ctypes.c_int64, P, P]
         L.kg_fill_evidence.argtypes = [ctypes.POINTER(KgCfg), ctypes.c_int64, ctypes.c_int64, P]
+        L.kg_fill_embeddings.argtypes = [ctypes.POINTER(KgCfg), ctypes.c_int64, ctypes.c_int64,
+                                         ctypes.c_int32, ctypes.c_int32, P, P, ctypes.c_int32]
         L.kg_fill_pool_host.argtypes = [ctypes.POINTER(KgCfg), P, ctypes.c_int64, P, P, P,
                                         ctypes.c_int32, ctypes.c_int32]
         L.kg_fill_pool_host.restype = ctypes.c_int
@@ -145,6 +147,15 @@ class GenSpec:
         c = self.cfg()
         lib().kg_fill_evidence(ctypes.byref(c), t0, n, _ptr(out))
         return out
+
+    def embeddings(self, t0: int, n: int, dim: int = 256, gamma: int = 2):
+        """(item bf16 bits [n][dim], op bf16 bits [n_ops][dim]) for the embedding stage."""
+        item = np.empty((n, dim), np.uint16)
+        op = np.empty((self.n_ops, dim), np.uint16)
+        c = self.cfg()
+        lib().kg_fill_embeddings(ctypes.byref(c), t0, n, dim, gamma, _ptr(item), _ptr(op),
+                                 max(1, min(16, os.cpu_count() or 1)))
+        return item, op
 
     def page_elems(self) -> int:
         return self.n_layers * 2 * self.n_kv_heads * PAGE * self.head_dim

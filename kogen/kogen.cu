@@ -199,6 +199,30 @@ void kg_fill_evidence(const kg_cfg* c, int64_t t0, int64_t n, int32_t* ev) {
   }
 }
 
+// item embeddings bf16 [n][dim] of tuples t0..t0+n-1 and operator embeddings bf16 [n_ops][dim]
+void kg_fill_embeddings(const kg_cfg* c, int64_t t0, int64_t n, int32_t dim, int32_t gamma,
+                        uint16_t* item, uint16_t* op, int32_t n_threads) {
+  std::vector<int32_t> edir((size_t)c->n_ops * dim);
+  for (int o = 0; o < c->n_ops; ++o)
+    for (int d = 0; d < dim; ++d) {
+      edir[(size_t)o * dim + d] = kg_edir(c, o, d);
+      if (op) op[(size_t)o * dim + d] = kg_bf16_of_int32nd(kg_clamp127(edir[(size_t)o * dim + d]));
+    }
+  if (!item) return;
+  if (n_threads < 1) n_threads = 1;
+  std::vector<std::thread> th;
+  for (int w = 0; w < n_threads; ++w)
+    th.emplace_back([&, w]() {
+      for (int64_t i = w; i < n; i += n_threads) {
+        kg_tuple tp;
+        kg_tuple_init(c, t0 + i, &tp);
+        for (int d = 0; d < dim; ++d)
+          item[(size_t)i * dim + d] = kg_bf16_of_int32nd(kg_emb_int(c, &tp, t0 + i, d, gamma));
+      }
+    });
+  for (auto& x : th) x.join();
+}
+
 // Host fill of the pages of tuples tuple_ids[0..n): tuple tuple_ids[i] owns logical pages
 // page_indptr[i] .. page_indptr[i+1] (ceil(L/16) of them) placed at physical page_ids[...].
 // pool has room for max(page_ids)+1 pages.  Multi-threaded over tuples.

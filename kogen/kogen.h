@@ -37,7 +37,8 @@
 /* tensor ids: separate hash streams */
 enum {
   KG_T_MU = 1, KG_T_QDIR = 2, KG_T_RHO = 3, KG_T_Q = 4, KG_T_W = 5,
-  KG_T_K = 6, KG_T_V = 7, KG_T_EVID = 8, KG_T_LABEL = 9, KG_T_LEN = 10
+  KG_T_K = 6, KG_T_V = 7, KG_T_EVID = 8, KG_T_LABEL = 9, KG_T_LEN = 10, KG_T_EMB = 11,
+  KG_T_EDIR = 12
 };
 
 typedef struct {
@@ -197,6 +198,20 @@ KG_HD int32_t kg_v_int(const kg_cfg* c, const kg_tuple* tp, uint64_t row_hash, i
   int32_t v = kg_nrm_at(row_hash, d);
   for (int32_t o = 0; o < c->n_ops; ++o)
     if (kg_is_evid(c, tp, o, i)) v += kg_fdiv(c->v_gamma * rho_lab[o], 32);
+  return kg_clamp127(v);
+}
+
+/* ---------------- item / operator embeddings (embedding-similarity stage, NEXT-3) --------
+ * op embedding e_o[d] = clamp(edir_o[d])/32; item embedding of tuple t:
+ * clamp(nrm + Σ_{filters o} ⌊γ_e · y_{t,o} · edir_o[d] / 32⌋)/32 with y = ±1 the latent label —
+ * a weaker, noisier signal than the KV-cache operators (a cheap first stage). */
+KG_HD int32_t kg_edir(const kg_cfg* c, int32_t o, int32_t d) {
+  return kg_nrm_at(kg_h(c->seed, KG_T_EDIR, (uint64_t)o, 0, 0, 0), d);
+}
+KG_HD int32_t kg_emb_int(const kg_cfg* c, const kg_tuple* tp, int64_t t, int32_t d, int32_t gamma) {
+  int32_t v = kg_nrm_at(kg_h(c->seed, KG_T_EMB, (uint64_t)t, 0, 0, 0), d);
+  for (int32_t o = 0; o < c->n_ops; ++o)
+    if (c->op_classes[o] <= 1) v += kg_fdiv(gamma * tp->label[o] * kg_edir(c, o, d), 32);
   return kg_clamp127(v);
 }
 

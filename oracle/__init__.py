@@ -166,3 +166,20 @@ def score_workload(wl, tuple_ids, n_threads: int = 0, variants=None, want_z=Fals
     ops = workload_ops(wl)
     return score(wl.spec, pool, indptr, ids, sl, ops, variants or wl.variants,
                  n_threads=n_threads, want_z=want_z)
+
+
+def embed_scores(item_bits: np.ndarray, op_bits: np.ndarray) -> np.ndarray:
+    """Embedding-similarity stage (NEXT-3): cosine similarity of every item
+    embedding with every operator embedding, fp64, by definition: ⟨e, q⟩ / (‖e‖ ‖q‖) (0 if a norm
+    is 0).  item_bits: bf16 bits [n][dim]; op_bits: bf16 bits [n_e][dim].  Returns [n_e][n]."""
+    def f(b):
+        return (np.asarray(b, np.uint32) << 16).view(np.float32).astype(np.float64)
+    e, q = f(item_bits), f(op_bits)
+    out = np.zeros((q.shape[0], e.shape[0]))
+    ne = np.sqrt((e * e).sum(axis=1))
+    for k in range(q.shape[0]):
+        nq = np.sqrt((q[k] * q[k]).sum())
+        dot = e @ q[k]
+        den = ne * nq
+        out[k] = np.where(den > 0, dot / np.where(den > 0, den, 1.0), 0.0)
+    return out

@@ -75,6 +75,8 @@ def _load():
     L.ko_workspace_size.restype = ctypes.c_size_t
     L.ko_beta_lower_bound.argtypes = [I64, I64, ctypes.c_double]
     L.ko_beta_lower_bound.restype = ctypes.c_double
+    L.ko_embed_scores.argtypes = [P, I32, I64, P, I32, P, I32, I32, I32, P, I64, P, P]
+    L.ko_embed_scores.restype = ctypes.c_int
     L.ko_soft_stats.argtypes = [P, P, P, ctypes.c_double, P, P, I32, I32, I64, P, P, P,
                                 ctypes.c_size_t, P]
     L.ko_soft_stats.restype = ctypes.c_int
@@ -89,7 +91,7 @@ def _load():
 
 _lib = _load()
 EXPORTS = ("ko_score_batch", "ko_route", "ko_reduce_stats", "ko_workspace_size",
-           "ko_soft_stats", "ko_soft_workspace_size", "ko_beta_lower_bound",
+           "ko_embed_scores", "ko_soft_stats", "ko_soft_workspace_size", "ko_beta_lower_bound",
            "ko_set_trace_events", "ko_last_error", "ko_version")
 
 
@@ -267,6 +269,22 @@ def reduce_stats(plans: Sequence[Sequence[Stage]], margins, classes, n_classes: 
                               nc, n_ops, n_var, n, _ptr(gold), counts.data_ptr(), _stream(stream))
     _check(rc)
     return counts
+
+
+EXTERNAL = (0, 0)  # variant whose margins the caller supplies (e.g. embed_scores)
+
+
+def embed_scores(item_emb, op_emb, op_ids: Sequence[int], margins, variant: int,
+                 tuple_idx=None, stream=None):
+    """ko_embed_scores: margins[op_ids[e]][variant][t] = cos(item_emb[t], op_emb[e])."""
+    n_ops, n_var, n = margins.shape
+    ids = (ctypes.c_int32 * len(op_ids))(*[int(x) for x in op_ids])
+    n_idx = 0 if tuple_idx is None else int(tuple_idx.numel())
+    rc = _lib.ko_embed_scores(item_emb.data_ptr(), int(item_emb.shape[1]), int(item_emb.shape[0]),
+                              op_emb.data_ptr(), int(op_emb.shape[0]), ids, n_ops, int(variant),
+                              n_var, _ptr(tuple_idx), n_idx, margins.data_ptr(), _stream(stream))
+    _check(rc)
+    return margins
 
 
 def soft_stats(plan: Sequence[Stage], pick_scores: Sequence[float], stage_cost: Sequence[float],

@@ -41,6 +41,10 @@ ko_status fail(ko_status st, const char* fmt, ...) {
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// external variant: margins supplied by the caller (keep‰ = 0, layer_cut = 0), e.g. an
+// embedding-similarity stage from ko_embed_scores
+inline bool is_external(const ko_variant& v) { return v.keep_permille == 0 && v.layer_cut == 0; }
+
 int pow2_at_least(int x) {
   int p = 1;
   while (p < x) p <<= 1;
@@ -79,6 +83,7 @@ ko_status validate_variants(const ko_kv_cache* kv, const ko_variant* v, int32_t 
   if (!v || n < 1 || n > KO_MAX_VARIANTS)
     return fail(KO_EINVAL, "n_variants %d outside [1,%d]", n, KO_MAX_VARIANTS);
   for (int i = 0; i < n; ++i) {
+    if (v[i].keep_permille == 0 && v[i].layer_cut == 0) continue;  // external (caller's margins)
     if (v[i].keep_permille < 1 || v[i].keep_permille > 1000)
       return fail(KO_EINVAL, "variant %d: keep_permille %d outside [1,1000]", i, v[i].keep_permille);
     if (v[i].layer_cut < 1 || v[i].layer_cut > kv->n_layers)
@@ -344,8 +349,12 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   if (n_plans > 0 && !plans) return fail(KO_EINVAL, "plans is NULL with n_plans > 0");
   int32_t ncls[KO_MAX_OPS] = {1, 1, 1, 1};
   for (int o = 0; o < n_ops; ++o) ncls[o] = ops[o].n_classes;
-  for (int g = 0; g < n_plans; ++g)
+  for (int g = 0; g < n_plans; ++g) {
     if ((st = validate_plan(&plans[g], g, ncls, n_ops, n_variants)) != KO_OK) return st;
+    for (int i = 0; i < plans[g].n_stages; ++i)
+      if (is_external(variants[plans[g].stage[i].variant]) && ncls[plans[g].stage[i].op] > 1)
+        return fail(KO_EUNSUPPORTED, "plan %d stage %d: external variant on a map operator", g, i);
+  }
   if (n_plans > 0 && !counts) return fail(KO_EINVAL, "counts is NULL with plans");
   if (tuple_idx && n_idx < 0) return fail(KO_EINVAL, "n_idx < 0");
   const bool routed = n_plans == 1;
@@ -366,14 +375,19 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
 
   if (!routed) {
     // ---- grid / profiling mode: all ops × all variants in one read, every plan per tuple
-    int op_sel[KO_MAX_OPS], var_sel[KO_MAX_VARIANTS];
+    int op_sel[KO_MAX_OPS], var_sel[KO_MAX_VARIANTS], n_int = 0, ext[KO_MAX_VARIANTS], n_ext = 0;
     for (int i = 0; i < n_ops; ++i) op_sel[i] = i;
-    for (int i = 0; i < n_variants; ++i) var_sel[i] = i;
+    for (int i = 0; i < n_variants; ++i) {
+      if (is_external(variants[i])) ext[n_ext++] = i; else var_sel[n_int++] = i;
+    }
+    if (n_int == 0) return fail(KO_EINVAL, "no KV variant to score (all variants external)");
     int CPR0 = 1, CPR1 = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
-    fill_common(sp, pp, kv, ops, op_sel, n_ops, variants, var_sel, n_variants, n_ops, n_variants,
+    fill_common(sp, pp, kv, ops, op_sel, n_ops, variants, var_sel, n_int, n_ops, n_variants,
                 ws, &CPR0, &CPR1);
+    sp.n_ext = n_ext;
+    for (int i = 0; i < n_ext; ++i) sp.ext_ids[i] = ext[i];
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
     sp.work = tuple_idx;
     sp.work_len_host = n_work;
@@ -397,8 +411,12 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
 
   // ---- routed mode (cascade execution): only tuples reaching a stage are scored
   const ko_plan& P = plans[0];
-  if (margins)
-    KO_CUDA(cudaMemsetAsync(margins, 0xFF, sizeof(float) * (size_t)n_ops * n_variants * kv->n_tuples, s));
+  if (margins)  // unreached entries read NaN; external variants are inputs and stay untouched
+    for (int o = 0; o < n_ops; ++o)
+      for (int v = 0; v < n_variants; ++v)
+        if (!is_external(variants[v]))
+          KO_CUDA(cudaMemsetAsync(margins + ((size_t)o * n_variants + v) * kv->n_tuples, 0xFF,
+                                  sizeof(float) * (size_t)kv->n_tuples, s));
   ko::RouteParams rp;
   std::memset(&rp, 0, sizeof(rp));
   rp.plan = P;
@@ -438,22 +456,32 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   int pv[KO_MAX_VARIANTS], n_pv = 0;
   bool seen_v[KO_MAX_VARIANTS] = {false};
   for (int i = 0; i < P.n_stages; ++i)
-    if (!seen_v[P.stage[i].variant]) { seen_v[P.stage[i].variant] = true; pv[n_pv++] = P.stage[i].variant; }
+    if (!seen_v[P.stage[i].variant] && !is_external(variants[P.stage[i].variant])) {
+      seen_v[P.stage[i].variant] = true;
+      pv[n_pv++] = P.stage[i].variant;
+    }
   std::stable_sort(pv, pv + n_pv, [&](int a, int b) {
     const int64_t ea = (int64_t)variants[a].keep_permille * variants[a].layer_cut;
     const int64_t eb = (int64_t)variants[b].keep_permille * variants[b].layer_cut;
     return ea < eb;
   });
   int var_rank[KO_MAX_VARIANTS];
-  for (int v = 0; v < KO_MAX_VARIANTS; ++v) var_rank[v] = 0;
+  for (int v = 0; v < KO_MAX_VARIANTS; ++v) var_rank[v] = (v < n_variants && is_external(variants[v])) ? -1 : 0;
   for (int k = 0; k < n_pv; ++k) var_rank[pv[k]] = k;
+  if (!margins) {
+    for (int i = 0; i < P.n_stages; ++i)
+      if (is_external(variants[P.stage[i].variant]))
+        return fail(KO_EINVAL, "routed plan uses an external variant but margins is NULL");
+  }
 
   // One launch per plan position (= stage): tuples are queued by their own plan walk to the
   // first later position that computes what they need, so one pass in plan order suffices.
   KO_CUDA(cudaMemsetAsync(ws.round_len, 0, sizeof(unsigned long long) * KO_MAX_STAGES, s));
   for (int pos = 0; pos < P.n_stages; ++pos) {
     const int g = group_of_op[P.stage[pos].op];
-    const int r = var_rank[P.stage[pos].variant];
+    // a stage on an external variant computes nothing itself; its launch still walks the
+    // tuples queued there (with rank 0 extents, never needed by them)
+    const int r = std::max(var_rank[P.stage[pos].variant], 0);
     int CPR0 = 1, CPR1 = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
@@ -588,6 +616,39 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
   rp.counts = (unsigned long long*)counts;
   for (int g = 0; g < n_plans; ++g) rp.plans[g] = plans[g];
   KO_CUDA(ko::launch_reduce(rp, (cudaStream_t)stream));
+  return KO_OK;
+}
+
+ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, const void* op_emb,
+                          int32_t n_emb, const int32_t* op_ids, int32_t n_ops, int32_t variant,
+                          int32_t n_variants, const int32_t* tuple_idx, int64_t n_idx,
+                          float* margins, void* stream) {
+  if (!item_emb || !op_emb || !op_ids || !margins) return fail(KO_EINVAL, "ko_embed_scores: NULL argument");
+  if (dim < 8 || dim % 8 != 0 || dim > 4096) return fail(KO_EINVAL, "dim %d: multiple of 8 in [8,4096]", dim);
+  if (n_emb < 1 || n_emb > KO_MAX_OPS) return fail(KO_EINVAL, "n_emb %d outside [1,%d]", n_emb, KO_MAX_OPS);
+  if (n_ops < 1 || n_ops > KO_MAX_OPS) return fail(KO_EINVAL, "n_ops %d", n_ops);
+  if (variant < 0 || variant >= n_variants || n_variants > KO_MAX_VARIANTS)
+    return fail(KO_EINVAL, "variant %d / n_variants %d", variant, n_variants);
+  if (n_tuples < 0 || (tuple_idx && n_idx < 0)) return fail(KO_EINVAL, "negative sizes");
+  if (((uintptr_t)item_emb & 15) != 0) return fail(KO_EINVAL, "item_emb not 16-byte aligned");
+  ko::EmbedParams ep;
+  std::memset(&ep, 0, sizeof(ep));
+  for (int i = 0; i < n_emb; ++i) {
+    if (op_ids[i] < 0 || op_ids[i] >= n_ops) return fail(KO_EINVAL, "op_ids[%d] = %d", i, op_ids[i]);
+    ep.op_ids[i] = op_ids[i];
+  }
+  ep.item_emb = (const uint16_t*)item_emb;
+  ep.op_emb = (const uint16_t*)op_emb;
+  ep.dim = dim;
+  ep.n_e = n_emb;
+  ep.variant = variant;
+  ep.n_variants = n_variants;
+  ep.n_tuples = n_tuples;
+  ep.tuple_idx = tuple_idx;
+  ep.n_idx = n_idx;
+  ep.margins = margins;
+  if ((tuple_idx ? n_idx : n_tuples) == 0) return KO_OK;
+  KO_CUDA(ko::launch_embed(ep, (cudaStream_t)stream));
   return KO_OK;
 }
 

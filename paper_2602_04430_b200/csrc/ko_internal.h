@@ -48,6 +48,8 @@ struct ScoreParams {
   int32_t rows_per_op;  // gqa * n_q
   int32_t slot_op[16];  // row slot (half*8 + g) → local op, -1 = padding
   int32_t n_ops_total, n_var_total;
+  int32_t n_ext;               // external variants (caller-supplied margins, keep‰ = 0)
+  int32_t ext_ids[kMaxVar];
   // variants of this launch
   int32_t n_var;
   int32_t keep[kMaxVar], cut[kMaxVar], var_ids[kMaxVar];
@@ -127,6 +129,20 @@ struct ReduceParams {
   unsigned long long* counts;
   ko_plan plans[kMaxPlans];
 };
+
+// embedding-similarity stage
+struct EmbedParams {
+  const uint16_t* item_emb;  // bf16 [n_tuples][dim]
+  const uint16_t* op_emb;    // bf16 [n_e][dim]
+  int32_t dim, n_e;
+  int32_t op_ids[kMaxOps];   // caller's op of each embedding
+  int32_t variant, n_variants;
+  int64_t n_tuples;
+  const int32_t* tuple_idx;
+  int64_t n_idx;
+  float* margins;            // [n_ops][n_variants][n_tuples]
+};
+cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s);
 
 // soft relaxation of one plan (ko_soft.cu)
 struct SoftParams {

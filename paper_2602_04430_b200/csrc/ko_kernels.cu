@@ -26,6 +26,8 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "ko_internal.h"
 
 namespace ko {
@@ -561,13 +563,22 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         p.wm[oi] = m;
         p.wc[oi] = cls;
       }
-      s_m[warp][p.op_ids[o] * p.n_var + v] = m;  // indexed by the caller's op, local variant
-      s_c[warp][p.op_ids[o] * p.n_var + v] = cls;
+      s_m[warp][p.op_ids[o] * p.n_var_total + p.var_ids[v]] = m;  // caller's op and variant
+      s_c[warp][p.op_ids[o] * p.n_var_total + p.var_ids[v]] = cls;
+    }
+    if (p.mode == MODE_GRID && p.n_ext) {
+      // external variants (margins supplied by the caller, e.g. ko_embed_scores) join the plans
+      for (int idx = lane; idx < p.n_ops_total * p.n_ext; idx += 32) {
+        const int o = idx / p.n_ext, v = p.ext_ids[idx % p.n_ext];
+        const size_t oi = ((size_t)o * p.n_var_total + v) * p.n_tuples + t;
+        s_m[warp][o * p.n_var_total + v] = __ldcg(p.margins + oi);
+        s_c[warp][o * p.n_var_total + v] = 0;
+      }
     }
     __syncwarp();
     if (p.mode == MODE_GRID) {
       for (int gp = lane; gp < p.n_plans; gp += 32)
-        eval_plan(p.plans[gp], s_m[warp], s_c[warp], p.n_var, p.op_classes_g, p.gold, p.n_tuples,
+        eval_plan(p.plans[gp], s_m[warp], s_c[warp], p.n_var_total, p.op_classes_g, p.gold, p.n_tuples,
                   t, s_cnt + gp * kCountsPerPlan);
     } else if (walk && lane == 0) {
       // Routed execution: this launch is plan position `pos` = (operator group, variant rank).
@@ -591,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         const int g = p.group_of_op[o];
         const int rk = p.var_rank[st.variant];
         const uint32_t have = (done >> (4 * g)) & 15u;      // 15: never computed
-        if (have == 15u || (int)have - 1 < rk) {
+        if (rk >= 0 && (have == 15u || (int)have - 1 < rk)) {  // rk < 0: external, always there
           // the next position computing (g, ≥ rk) exists: stage s itself is one (s > pos)
           int q = p.pos + 1;
           while (q < p.n_pos && !(p.pos_group[q] == g && p.pos_round[q] >= rk)) ++q;
@@ -604,15 +615,20 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         const size_t oi = ((size_t)o * p.n_var_total + st.variant) * p.n_tuples + t;
         float m;
         int32_t cls;
-        if (g == p.group) {
-          m = s_m[warp][o * p.n_var + p.var_local[st.variant]];
-          cls = s_c[warp][o * p.n_var + p.var_local[st.variant]];
+        if (rk < 0) {                 // external variant: the caller's margin (filters only)
+          m = __ldcg(p.margins + oi);
+          cls = 0;
+        } else if (g == p.group) {
+          m = s_m[warp][o * p.n_var_total + st.variant];
+          cls = s_c[warp][o * p.n_var_total + st.variant];
         } else {
           m = __ldcg(p.wm + oi);
           cls = __ldcg(p.wc + oi);
         }
-        if (p.margins) p.margins[oi] = m;
-        if (p.classes) p.classes[oi] = cls;
+        if (rk >= 0) {
+          if (p.margins) p.margins[oi] = m;
+          if (p.classes) p.classes[oi] = cls;
+        }
         int* cnt = s_cnt + 5 + 4 * s;
         atomicAdd(&cnt[0], 1);
         const int d = decide(m, st, p.op_classes_g[o]);
@@ -923,7 +939,74 @@ cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// Embedding-similarity filter stage (Blip): cosine of each item
+// embedding with each operator embedding.  One warp per tuple, 16-byte loads, fp32 accumulate;
+// HBM-bound GEMV (the operator embeddings live in shared memory).
+// ------------------------------------------------------------------------------------------
+__global__ void embed_kernel(const __grid_constant__ EmbedParams p) {
+  extern __shared__ float s_op[];  // [n_e][dim] fp32, then [n_e] norms
+  const int dim = p.dim;
+  for (int i = threadIdx.x; i < p.n_e * dim; i += blockDim.x)
+    s_op[i] = __bfloat162float(__ushort_as_bfloat16(p.op_emb[i]));
+  __syncthreads();
+  float* s_norm = s_op + p.n_e * dim;
+  if (threadIdx.x < p.n_e) {
+    float acc = 0.f;
+    for (int d = 0; d < dim; ++d) acc = fmaf(s_op[threadIdx.x * dim + d], s_op[threadIdx.x * dim + d], acc);
+    s_norm[threadIdx.x] = sqrtf(acc);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n = p.tuple_idx ? p.n_idx : p.n_tuples;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += nw) {
+    const int64_t t = p.tuple_idx ? p.tuple_idx[w] : w;
+    const uint16_t* e = p.item_emb + (size_t)t * dim;
+    float dot[KO_MAX_OPS] = {0.f, 0.f, 0.f, 0.f};
+    float nn = 0.f;
+    for (int d0 = lane * 8; d0 < dim; d0 += 256) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(e + d0));
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float x = __uint_as_float((k & 1 ? wv[k >> 1] & 0xFFFF0000u : wv[k >> 1] << 16));
+        nn = fmaf(x, x, nn);
+#pragma unroll
+        for (int o = 0; o < KO_MAX_OPS; ++o)
+          if (o < p.n_e) dot[o] = fmaf(x, s_op[o * dim + d0 + k], dot[o]);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      nn += __shfl_xor_sync(0xffffffffu, nn, off);
+#pragma unroll
+      for (int o = 0; o < KO_MAX_OPS; ++o) dot[o] += __shfl_xor_sync(0xffffffffu, dot[o], off);
+    }
+    if (lane < p.n_e) {
+      float d = dot[0];
+#pragma unroll
+      for (int o = 1; o < KO_MAX_OPS; ++o) if (lane == o) d = dot[o];
+      const float den = sqrtf(nn) * s_norm[lane];
+      p.margins[((size_t)p.op_ids[lane] * p.n_variants + p.variant) * p.n_tuples + t] =
+          den > 0.f ? __fdiv_rn(d, den) : 0.f;
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s) {
+  const size_t smem = sizeof(float) * ((size_t)p.n_e * p.dim + p.n_e);
+  const int64_t n = p.tuple_idx ? p.n_idx : p.n_tuples;
+  int64_t blocks = (n + 7) / 8;
+  blocks = std::min<int64_t>(blocks, (int64_t)num_sms() * 8);
+  if (blocks < 1) blocks = 1;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(embed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  embed_kernel<<<(unsigned)blocks, 256, smem, s>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t s) {
   prep_kernel<<<num_sms() * 2, 256, 0, s>>>(p);
