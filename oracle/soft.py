@@ -81,7 +81,7 @@ def soft_stats(plan: Sequence[Tuple], pick: Sequence[float], tau: float, margins
     gt = torch.from_numpy(np.asarray(gold, np.float64))
     ct = [float(c) for c in stage_cost]
     outs = soft_forward(plan, s, lo, hi, tau, mt, gt, ct)
-    vals = np.array([float(x) for x in outs])
+    vals = np.array([float(x.detach()) for x in outs])
     jac = np.zeros((4, 3 * S))
     for k, out in enumerate(outs):
         gs, gl, gh = torch.autograd.grad(out, (s, lo, hi), retain_graph=True, allow_unused=True)
