@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU work budget of the oracle sample (cpu_baseline / reference arm)")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--mode", default="pass", choices=["pass", "soft", "embed"],
+                    help="pass: the hot path (default); soft / embed: NEXT-1 / NEXT-3 kernels")
     return ap.parse_args()
 
 
@@ -224,6 +226,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.mode != "pass":
+        run_next(args)
+        return
 
     import torch
     import paper_2602_04430_b200 as ko
@@ -345,6 +350,69 @@ def main():
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def _time(fn, steps, warmup):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_next(args):
+    """Supplementary lines for the NEXT rows (not the driver's default): the soft relaxation of a
+    C5 plan on the margins of a real C5 pass (NEXT-1), and the embedding-similarity stage over
+    1 M tuples × 256 dims (NEXT-3)."""
+    import torch
+    import paper_2602_04430_b200 as ko
+    from kogen import workloads
+    from kogen.device import device_workload
+    peak, peak_src = measured_peak()
+    if args.mode == "soft":
+        wl = workloads.get("C5")
+        n = args.n_tuples or wl.bench_n
+        d = device_workload(wl, n=n, placement="contiguous")
+        m, c, _ = ko.score_batch(d["kv"], d["ops"], wl.variants)
+        plan = wl.plans[9]
+        S = len(plan)
+        pick = [0.3, 0.0, -0.2, 0.0][:S]
+        cost = [0.25, 1.0, 0.25, 1.0][:S]
+        out = torch.empty(4 + 12 * S, dtype=torch.float64, device="cuda")
+        ws = torch.empty(int(ko.lib().ko_soft_workspace_size(S, n)), dtype=torch.uint8, device="cuda")
+        ms = _time(lambda: ko.soft_stats(plan, pick, cost, 0.1, m, wl.spec.op_classes,
+                                         gold=d["gold"], out=out, workspace=ws),
+                   args.steps, args.warmup)
+        items = (3 * S + 1) * n
+        traffic = items * 4 * 8 * 2 + (3 * S + 1) * n * (S * 4 + wl.spec.n_ops)
+        line = {"mode": "soft", "metric": "soft-relaxation evaluations (value + Jacobian) / s",
+                "value": 1000.0 / ms, "unit": "evals/s", "ms_per_step": ms, "n_tuples": n,
+                "n_stages": S, "params": 3 * S, "tuple_params_per_s": items / (ms / 1000.0),
+                "workspace_gbs": traffic / (ms / 1000.0) / 1e9, "peak_gbs": peak,
+                "config": {"workload": "C5 margins (50k tuples), plan " + str(plan)}}
+    else:
+        wl = workloads.get("C5")
+        n = args.n_tuples or 1_000_000
+        dim = 256
+        item, op = wl.spec.embeddings(0, n, dim)
+        di = torch.from_numpy(item.view(np.int16)).cuda().view(torch.bfloat16)
+        dq = torch.from_numpy(op.view(np.int16)).cuda().view(torch.bfloat16)
+        m = torch.empty((2, 1, n), device="cuda")
+        ms = _time(lambda: ko.embed_scores(di, dq, [0, 1], m, variant=0), args.steps, args.warmup)
+        alg = n * dim * 2 + n * 2 * 4
+        line = {"mode": "embed", "metric": "embedding-similarity scores / s", "unit": "tuples/s",
+                "value": n / (ms / 1000.0), "ms_per_step": ms,
+                "roofline": {"bound": "hbm", "achieved": alg / (ms / 1000.0) / 1e9, "peak": peak,
+                             "unit": "GB/s", "frac": alg / (ms / 1000.0) / 1e9 / peak,
+                             "peak_source": peak_src},
+                "config": {"workload": f"{n} tuples x {dim}-d bf16 item embeddings, 2 operators"}}
+    print(json.dumps(line), flush=True)
 
 
 def run_e2e(args, ko, torch, wl, d, ops, gold, plans, margins, classes, counts, ws, world, dist):

@@ -189,7 +189,7 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
  * threshold", P:456-458 two thresholds, Blip P:746; NEXT-3): for every tuple t (tuple_idx or all)
  * and every operator embedding e, margins[op_ids[e]][variant][t] = cos(item_emb[t], op_emb[e]).
  * item_emb: device bf16 [n_tuples][dim] (16-byte aligned); op_emb: device bf16 [n_emb][dim];
- * op_ids: host int32 [n_emb]; dim a multiple of 8 (≤ 4096); fp32 accumulation.  Use a variant
+ * op_ids: host int32 [n_emb]; dim a multiple of 8 (≤ 1024); fp32 accumulation.  Use a variant
  * marked external (keep‰ = layer_cut = 0) to chain it into plans.                              */
 ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, const void* op_emb,
                           int32_t n_emb, const int32_t* op_ids, int32_t n_ops, int32_t variant,

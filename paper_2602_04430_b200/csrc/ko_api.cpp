@@ -624,7 +624,7 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
                           int32_t n_variants, const int32_t* tuple_idx, int64_t n_idx,
                           float* margins, void* stream) {
   if (!item_emb || !op_emb || !op_ids || !margins) return fail(KO_EINVAL, "ko_embed_scores: NULL argument");
-  if (dim < 8 || dim % 8 != 0 || dim > 4096) return fail(KO_EINVAL, "dim %d: multiple of 8 in [8,4096]", dim);
+  if (dim < 8 || dim % 8 != 0 || dim > 1024) return fail(KO_EINVAL, "dim %d: multiple of 8 in [8,1024]", dim);
   if (n_emb < 1 || n_emb > KO_MAX_OPS) return fail(KO_EINVAL, "n_emb %d outside [1,%d]", n_emb, KO_MAX_OPS);
   if (n_ops < 1 || n_ops > KO_MAX_OPS) return fail(KO_EINVAL, "n_ops %d", n_ops);
   if (variant < 0 || variant >= n_variants || n_variants > KO_MAX_VARIANTS)

@@ -944,52 +944,83 @@ cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t
 // embedding with each operator embedding.  One warp per tuple, 16-byte loads, fp32 accumulate;
 // HBM-bound GEMV (the operator embeddings live in shared memory).
 // ------------------------------------------------------------------------------------------
-__global__ void embed_kernel(const __grid_constant__ EmbedParams p) {
-  extern __shared__ float s_op[];  // [n_e][dim] fp32, then [n_e] norms
-  const int dim = p.dim;
-  for (int i = threadIdx.x; i < p.n_e * dim; i += blockDim.x)
-    s_op[i] = __bfloat162float(__ushort_as_bfloat16(p.op_emb[i]));
-  __syncthreads();
-  float* s_norm = s_op + p.n_e * dim;
-  if (threadIdx.x < p.n_e) {
-    float acc = 0.f;
-    for (int d = 0; d < dim; ++d) acc = fmaf(s_op[threadIdx.x * dim + d], s_op[threadIdx.x * dim + d], acc);
-    s_norm[threadIdx.x] = sqrtf(acc);
-  }
-  __syncthreads();
+// Each lane owns 8 consecutive dims of every 256-dim chunk; the operator embeddings of its dims
+// stay in registers, 4 tuples are in flight per warp, and one xor-tree per tuple and output
+// finishes the dot products.
+template <int CH>  // 256-dim chunks per embedding (dim ≤ 256·CH)
+__global__ void __launch_bounds__(256) embed_kernel(const __grid_constant__ EmbedParams p) {
   const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t n = p.tuple_idx ? p.n_idx : p.n_tuples;
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += nw) {
-    const int64_t t = p.tuple_idx ? p.tuple_idx[w] : w;
-    const uint16_t* e = p.item_emb + (size_t)t * dim;
-    float dot[KO_MAX_OPS] = {0.f, 0.f, 0.f, 0.f};
-    float nn = 0.f;
-    for (int d0 = lane * 8; d0 < dim; d0 += 256) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(e + d0));
-      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+  const int dim = p.dim;
+  float qv[KO_MAX_OPS][CH][8];
+  float qn[KO_MAX_OPS];
+#pragma unroll
+  for (int o = 0; o < KO_MAX_OPS; ++o) {
+    float acc = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const float x = __uint_as_float((k & 1 ? wv[k >> 1] & 0xFFFF0000u : wv[k >> 1] << 16));
-        nn = fmaf(x, x, nn);
+        const int d = ch * 256 + lane * 8 + k;
+        const float x = (o < p.n_e && d < dim)
+                            ? __bfloat162float(__ushort_as_bfloat16(p.op_emb[(size_t)o * dim + d]))
+                            : 0.f;
+        qv[o][ch][k] = x;
+        acc = fmaf(x, x, acc);
+      }
 #pragma unroll
-        for (int o = 0; o < KO_MAX_OPS; ++o)
-          if (o < p.n_e) dot[o] = fmaf(x, s_op[o * dim + d0 + k], dot[o]);
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    qn[o] = sqrtf(acc);
+  }
+  constexpr int TB = 4;  // tuples per warp iteration
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n = p.tuple_idx ? p.n_idx : p.n_tuples;
+  for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * TB; w0 < n;
+       w0 += nw * TB) {
+    uint4 v[TB][CH];
+    int64_t tt[TB];
+#pragma unroll
+    for (int b = 0; b < TB; ++b) {
+      const int64_t w = w0 + b;
+      tt[b] = w < n ? (p.tuple_idx ? (int64_t)p.tuple_idx[w] : w) : -1;
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) {
+        const int d0 = ch * 256 + lane * 8;
+        v[b][ch] = (tt[b] >= 0 && d0 < dim)
+                       ? __ldg(reinterpret_cast<const uint4*>(p.item_emb + (size_t)tt[b] * dim + d0))
+                       : make_uint4(0, 0, 0, 0);
       }
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      nn += __shfl_xor_sync(0xffffffffu, nn, off);
+    for (int b = 0; b < TB; ++b) {
+      float dot[KO_MAX_OPS] = {0.f, 0.f, 0.f, 0.f};
+      float nn = 0.f;
 #pragma unroll
-      for (int o = 0; o < KO_MAX_OPS; ++o) dot[o] += __shfl_xor_sync(0xffffffffu, dot[o], off);
-    }
-    if (lane < p.n_e) {
-      float d = dot[0];
+      for (int ch = 0; ch < CH; ++ch) {
+        const uint32_t wv[4] = {v[b][ch].x, v[b][ch].y, v[b][ch].z, v[b][ch].w};
 #pragma unroll
-      for (int o = 1; o < KO_MAX_OPS; ++o) if (lane == o) d = dot[o];
-      const float den = sqrtf(nn) * s_norm[lane];
-      p.margins[((size_t)p.op_ids[lane] * p.n_variants + p.variant) * p.n_tuples + t] =
-          den > 0.f ? __fdiv_rn(d, den) : 0.f;
+        for (int k = 0; k < 8; ++k) {
+          const float x = __uint_as_float(k & 1 ? wv[k >> 1] & 0xFFFF0000u : wv[k >> 1] << 16);
+          nn = fmaf(x, x, nn);
+#pragma unroll
+          for (int o = 0; o < KO_MAX_OPS; ++o) dot[o] = fmaf(x, qv[o][ch][k], dot[o]);
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        nn += __shfl_xor_sync(0xffffffffu, nn, off);
+#pragma unroll
+        for (int o = 0; o < KO_MAX_OPS; ++o)
+          if (o < p.n_e) dot[o] += __shfl_xor_sync(0xffffffffu, dot[o], off);
+      }
+      if (tt[b] >= 0 && lane < p.n_e) {
+        float d = dot[0], qq = qn[0];
+#pragma unroll
+        for (int o = 1; o < KO_MAX_OPS; ++o)
+          if (lane == o) { d = dot[o]; qq = qn[o]; }
+        const float den = sqrtf(nn) * qq;
+        p.margins[((size_t)p.op_ids[lane] * p.n_variants + p.variant) * p.n_tuples + tt[b]] =
+            den > 0.f ? __fdiv_rn(d, den) : 0.f;
+      }
     }
   }
 }
@@ -997,14 +1028,14 @@ __global__ void embed_kernel(const __grid_constant__ EmbedParams p) {
 }  // namespace
 
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s) {
-  const size_t smem = sizeof(float) * ((size_t)p.n_e * p.dim + p.n_e);
   const int64_t n = p.tuple_idx ? p.n_idx : p.n_tuples;
-  int64_t blocks = (n + 7) / 8;
+  int64_t blocks = (n + 31) / 32;  // 8 warps × 4 tuples
   blocks = std::min<int64_t>(blocks, (int64_t)num_sms() * 8);
   if (blocks < 1) blocks = 1;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(embed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  embed_kernel<<<(unsigned)blocks, 256, smem, s>>>(p);
+  const int ch = (p.dim + 255) / 256;
+  if (ch <= 1) embed_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(p);
+  else if (ch <= 2) embed_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(p);
+  else embed_kernel<4><<<(unsigned)blocks, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 
