@@ -63,6 +63,8 @@ def lib():
         L.oracle_run_plans.argtypes = [P, ctypes.c_int32, P, P, P, ctypes.c_int32, ctypes.c_int32,
                                        ctypes.c_int64, P, P, P]
         L.oracle_run_plans.restype = ctypes.c_int
+        L.oracle_build_order.argtypes = [ctypes.POINTER(OrKV), P, P, P, P, ctypes.c_int32]
+        L.oracle_build_order.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -183,3 +185,25 @@ def embed_scores(item_bits: np.ndarray, op_bits: np.ndarray) -> np.ndarray:
         den = ne * nq
         out[k] = np.where(den > 0, dot / np.where(den > 0, den, 1.0), 0.0)
     return out
+
+
+def build_order(geom, pool, indptr, page_ids, seq_len, mu, sigma2, dst_page_ids,
+                n_threads: int = 0) -> np.ndarray:
+    """Offline importance-ordered cache builder (NEXT-4, see ko_oracle.cpp): returns a new pool
+    (uint16 bf16 bits, same shape) whose pages dst_page_ids (same CSR indptr) hold each tuple's
+    tokens in descending expected-attention score per (layer, kv-head)."""
+    pool = np.ascontiguousarray(pool, np.uint16)
+    indptr = np.ascontiguousarray(indptr, np.int64)
+    page_ids = np.ascontiguousarray(page_ids, np.int32)
+    seq_len = np.ascontiguousarray(seq_len, np.int32)
+    mu = np.ascontiguousarray(mu, np.float32)
+    sigma2 = np.ascontiguousarray(sigma2, np.float32)
+    dst_ids = np.ascontiguousarray(dst_page_ids, np.int32)
+    kv = OrKV(geom.n_layers, geom.n_kv_heads, geom.gqa, geom.head_dim, geom.n_q,
+              pool.ctypes.data, pool.shape[0], indptr.ctypes.data, page_ids.ctypes.data,
+              seq_len.ctypes.data, len(seq_len))
+    dst = np.zeros_like(pool)
+    nt = n_threads or max(1, len(os.sched_getaffinity(0)))
+    rc = lib().oracle_build_order(ctypes.byref(kv), _p(mu), _p(sigma2), _p(dst), _p(dst_ids), nt)
+    assert rc == 0
+    return dst

@@ -21,6 +21,7 @@
 //   counts : TP/FP/FN of Eqs (sample-tp/fp/fn), applied to the whole plan output
 //            vs the gold plan, with map output-tuple semantics P:513-519;
 //            per-stage n_in / n_acc / n_rej / n_uns (selectivities P:541-547, cost Eq. P:338).
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -260,3 +261,66 @@ int oracle_run_plans(const or_plan* plans, int32_t n_plans, const double* margin
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// Offline importance-ordered cache builder (NEXT-4; KV caches are created
+// offline and compressed with query-agnostic Expected Attention, "select tokens based on their
+// expected contribution to attention across potential future queries").  Reading (DESIGN
+// §2, Q25): with a Gaussian query model q ~ N(μ, diag σ²) per (layer, kv-head), the log expected
+// un-normalised attention of key k is
+//     s(k) = (Σ_d μ_d k_d) / sqrt(D) + (Σ_d σ²_d k_d²) / (2 D),
+// evaluated in fp64, left to right, one rounding per operation (no fused multiply-add), so the
+// GPU builder takes identical decisions.  Tokens are stored in descending s (ties: lower original
+// index first); token of rank r goes to slot r % 16 of logical page r / 16.
+// ---------------------------------------------------------------------------------------------
+extern "C" int oracle_build_order(const or_kv* kv, const float* mu, const float* sigma2,
+                                  uint16_t* dst_pool, const int32_t* dst_page_ids,
+                                  int32_t n_threads) {
+  const int32_t D = kv->head_dim, H = kv->n_kv_heads, Lyr = kv->n_layers;
+  const double inv_sqrt_d = 1.0 / std::sqrt((double)D), inv_2d = 1.0 / (2.0 * (double)D);
+  if (n_threads < 1) n_threads = 1;
+  std::vector<std::thread> th;
+  for (int w = 0; w < n_threads; ++w)
+    th.emplace_back([&, w]() {
+      std::vector<double> sc;
+      std::vector<int32_t> order;
+      for (int64_t t = w; t < kv->n_tuples; t += n_threads) {
+        const int32_t L = kv->seq_len[t];
+        for (int32_t l = 0; l < Lyr; ++l)
+          for (int32_t h = 0; h < H; ++h) {
+            const float* m = mu + ((size_t)l * H + h) * D;
+            const float* s2 = sigma2 + ((size_t)l * H + h) * D;
+            sc.assign(L, 0.0);
+            order.resize(L);
+            for (int32_t i = 0; i < L; ++i) {
+              const uint16_t* k = kv_row(kv, t, l, 0, h, i);
+              double a = 0.0, b = 0.0;
+              for (int32_t d = 0; d < D; ++d) {
+                const double x = bf16_to_double(k[d]);
+                const double pa = (double)m[d] * x;
+                a = a + pa;
+                const double xx = x * x;
+                const double pb = (double)s2[d] * xx;
+                b = b + pb;
+              }
+              const double ta = a * inv_sqrt_d;
+              const double tb = b * inv_2d;
+              sc[i] = ta + tb;
+              order[i] = i;
+            }
+            std::stable_sort(order.begin(), order.end(),
+                             [&](int32_t x, int32_t y) { return sc[x] > sc[y]; });
+            for (int32_t r = 0; r < L; ++r) {
+              const int64_t page = dst_page_ids[kv->page_indptr[t] + r / 16];
+              for (int which = 0; which < 2; ++which) {
+                const uint16_t* src = kv_row(kv, t, l, which, h, order[r]);
+                uint16_t* dst = dst_pool + (((((size_t)page * Lyr + l) * 2 + which) * H + h) * 16 + r % 16) * D;
+                std::memcpy(dst, src, sizeof(uint16_t) * D);
+              }
+            }
+          }
+      }
+    });
+  for (auto& x : th) x.join();
+  return 0;
+}
