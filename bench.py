@@ -44,8 +44,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU work budget of the oracle sample (cpu_baseline / reference arm)")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--mode", default="pass", choices=["pass", "soft", "embed"],
-                    help="pass: the hot path (default); soft / embed: NEXT-1 / NEXT-3 kernels")
+    ap.add_argument("--mode", default="pass", choices=["pass", "soft", "embed", "build"],
+                    help="pass: the hot path (default); soft / embed / build: NEXT-1/3/4 kernels")
     return ap.parse_args()
 
 
@@ -396,6 +396,25 @@ def run_next(args):
                 "n_stages": S, "params": 3 * S, "tuple_params_per_s": items / (ms / 1000.0),
                 "workspace_gbs": traffic / (ms / 1000.0) / 1e9, "peak_gbs": peak,
                 "config": {"workload": "C5 margins (50k tuples), plan " + str(plan)}}
+    elif args.mode == "build":
+        wl = workloads.get("C2")
+        n = args.n_tuples or 2000
+        d = device_workload(wl, n=n, placement="contiguous")
+        kv = d["kv"]
+        g = torch.Generator().manual_seed(0)
+        mu = torch.randn((wl.spec.n_layers, wl.spec.n_kv_heads, wl.spec.head_dim), generator=g).cuda()
+        s2 = torch.rand((wl.spec.n_layers, wl.spec.n_kv_heads, wl.spec.head_dim), generator=g).cuda()
+        dst = torch.empty_like(kv.pool)
+        ms = _time(lambda: ko.build_importance_order(kv, mu, s2, dst, kv.page_ids),
+                   args.steps, args.warmup)
+        kvb = int(d["indptr"][-1]) * wl.spec.page_bytes()
+        alg = 2 * kvb + kvb // 2          # read K,V + write K,V (+ K read again for the scores)
+        line = {"mode": "build", "metric": "tuples ordered by expected attention / s",
+                "unit": "tuples/s", "value": n / (ms / 1000.0), "ms_per_step": ms,
+                "roofline": {"bound": "hbm", "achieved": alg / (ms / 1000.0) / 1e9, "peak": peak,
+                             "unit": "GB/s", "frac": alg / (ms / 1000.0) / 1e9 / peak,
+                             "peak_source": peak_src},
+                "config": {"workload": f"C2 geometry, {n} tuples x 512 tokens, {kvb} B of KV"}}
     else:
         wl = workloads.get("C5")
         n = args.n_tuples or 1_000_000

@@ -196,6 +196,19 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
                           int32_t n_variants, const int32_t* tuple_idx, int64_t n_idx,
                           float* margins, void* stream);
 
+/* ko_build_importance_order — offline builder of the importance-ordered store the variants read
+ * (NEXT-4; "KV Cache Creation", query-agnostic Expected Attention P:190-193).
+ * For every tuple, layer and kv-head of `src` (any token order), the log expected un-normalised
+ * attention of each key under a Gaussian query model N(mu, diag sigma2) (reading Q25),
+ *     s(k) = (Σ_d mu_d k_d)/sqrt(D) + (Σ_d sigma2_d k_d²)/(2D)   (fp64, no fused multiply-add),
+ * orders the tokens by descending s (ties: lower source index first) and writes their K and V
+ * rows, rank r to slot r % 16 of logical page r / 16, into dst_pool at pages dst_page_ids (same
+ * CSR offsets src->page_indptr; same page geometry).  Slots past L_t are not written.
+ * mu, sigma2: device fp32 [n_layers][n_kv_heads][head_dim].  Tuples longer than 4096 tokens are
+ * skipped (not supported).  Asynchronous on `stream`.                                         */
+ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, const float* sigma2,
+                                    void* dst_pool, const int32_t* dst_page_ids, void* stream);
+
 /* ko_soft_stats — the continuous relaxation of one plan (NEXT-1 of SURVEY §8(f)) on
  * precomputed margins: pick factors σ_i = sigmoid(s_i/τ) (final stages σ = 1), soft decisions
  * π_i = softmax([m − θ⁺, θ⁻ − m, 0]/τ) (final stages: accept = sigmoid((m − θ⁺)/τ)), the relaxed

@@ -75,6 +75,8 @@ def _load():
     L.ko_workspace_size.restype = ctypes.c_size_t
     L.ko_beta_lower_bound.argtypes = [I64, I64, ctypes.c_double]
     L.ko_beta_lower_bound.restype = ctypes.c_double
+    L.ko_build_importance_order.argtypes = [ctypes.POINTER(_KV), P, P, P, P, P]
+    L.ko_build_importance_order.restype = ctypes.c_int
     L.ko_embed_scores.argtypes = [P, I32, I64, P, I32, P, I32, I32, I32, P, I64, P, P]
     L.ko_embed_scores.restype = ctypes.c_int
     L.ko_soft_stats.argtypes = [P, P, P, ctypes.c_double, P, P, I32, I32, I64, P, P, P,
@@ -91,7 +93,7 @@ def _load():
 
 _lib = _load()
 EXPORTS = ("ko_score_batch", "ko_route", "ko_reduce_stats", "ko_workspace_size",
-           "ko_embed_scores", "ko_soft_stats", "ko_soft_workspace_size", "ko_beta_lower_bound",
+           "ko_embed_scores", "ko_build_importance_order", "ko_soft_stats", "ko_soft_workspace_size", "ko_beta_lower_bound",
            "ko_set_trace_events", "ko_last_error", "ko_version")
 
 
@@ -269,6 +271,16 @@ def reduce_stats(plans: Sequence[Sequence[Stage]], margins, classes, n_classes: 
                               nc, n_ops, n_var, n, _ptr(gold), counts.data_ptr(), _stream(stream))
     _check(rc)
     return counts
+
+
+def build_importance_order(src: KVCache, mu, sigma2, dst_pool, dst_page_ids, stream=None):
+    """ko_build_importance_order: dst_pool (same geometry, pages dst_page_ids under the same
+    CSR) receives every tuple's tokens in descending expected-attention order."""
+    rc = _lib.ko_build_importance_order(ctypes.byref(src._c()), mu.data_ptr(), sigma2.data_ptr(),
+                                        dst_pool.data_ptr(), dst_page_ids.data_ptr(),
+                                        _stream(stream))
+    _check(rc)
+    return dst_pool
 
 
 EXTERNAL = (0, 0)  # variant whose margins the caller supplies (e.g. embed_scores)

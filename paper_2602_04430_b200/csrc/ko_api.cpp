@@ -652,6 +652,35 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
   return KO_OK;
 }
 
+ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, const float* sigma2,
+                                    void* dst_pool, const int32_t* dst_page_ids, void* stream) {
+  ko_status st;
+  if ((st = validate_kv(src)) != KO_OK) return st;
+  if (!mu || !sigma2 || !dst_pool || !dst_page_ids)
+    return fail(KO_EINVAL, "ko_build_importance_order: NULL mu/sigma2/dst_pool/dst_page_ids");
+  if (((uintptr_t)dst_pool & 15) != 0) return fail(KO_EINVAL, "dst_pool not 16-byte aligned");
+  if (src->n_tuples == 0) return KO_OK;
+  ko::BuildParams bp;
+  std::memset(&bp, 0, sizeof(bp));
+  bp.src_pool = (const uint16_t*)src->kv_pool;
+  bp.indptr = src->page_indptr;
+  bp.src_ids = src->page_ids;
+  bp.seq_len = src->seq_len;
+  bp.n_tuples = src->n_tuples;
+  bp.n_layers = src->n_layers;
+  bp.n_kv_heads = src->n_kv_heads;
+  bp.head_dim = src->head_dim;
+  bp.page_elems = (int64_t)src->n_layers * 2 * src->n_kv_heads * KO_PAGE_TOKENS * src->head_dim;
+  bp.mu = mu;
+  bp.sigma2 = sigma2;
+  bp.dst_pool = (uint16_t*)dst_pool;
+  bp.dst_ids = dst_page_ids;
+  bp.inv_sqrt_d = 1.0 / std::sqrt((double)src->head_dim);
+  bp.inv_2d = 1.0 / (2.0 * (double)src->head_dim);
+  KO_CUDA(ko::launch_build(bp, (cudaStream_t)stream));
+  return KO_OK;
+}
+
 size_t ko_soft_workspace_size(int32_t n_stages, int64_t n_tuples) {
   if (n_stages < 1 || n_stages > KO_MAX_STAGES || n_tuples < 0) return 0;
   return align256(sizeof(double) * (size_t)(3 * n_stages + 1) * 4 * (size_t)std::max<int64_t>(n_tuples, 1));

@@ -1,0 +1,139 @@
+// ko_build.cu — offline importance-ordered KV-cache builder (NEXT-4).
+//
+// The paper prefills every item once and compresses its cache with query-agnostic Expected
+// Attention.  The variant knob of this library (keep‰ = a prefix) needs each tuple's
+// tokens stored in descending expected attention per (layer, kv-head) (Q2).  This kernel builds
+// such a store from a cache in natural token order: one CTA per (tuple, layer, kv-head)
+//   1. s_i = (Σ_d μ_d k_d)/√D + (Σ_d σ²_d k_d²)/(2D) for every token (Q25), fp64, left to right,
+//      one rounding per operation (__dmul_rn/__dadd_rn: no fused multiply-add), so the order is
+//      decided exactly as the oracle decides it;
+//   2. bitonic sort of (s desc, index asc) in shared memory (L ≤ 4096);
+//   3. gather: the K and V rows of rank r go to slot r % 16 of logical page r / 16 of the
+//      destination CSR, 16-byte copies.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <algorithm>
+
+#include "ko_internal.h"
+
+namespace ko {
+namespace {
+
+constexpr int kBuildThreads = 256;
+constexpr int kBuildMaxTokens = 4096;
+
+__device__ __forceinline__ double bf16_to_double(uint16_t b) {
+  return (double)__uint_as_float((uint32_t)b << 16);
+}
+
+// a precedes b: higher score first, then lower original index
+__device__ __forceinline__ bool precedes(double ka, int ia, double kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+__global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_constant__ BuildParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* key = reinterpret_cast<double*>(smem);                  // [N]
+  int* idx = reinterpret_cast<int*>(key + kBuildMaxTokens);       // [N]
+  float* s_mu = reinterpret_cast<float*>(idx + kBuildMaxTokens);  // [D]
+  float* s_s2 = s_mu + p.head_dim;                                // [D]
+  const int D = p.head_dim, H = p.n_kv_heads, Lyr = p.n_layers;
+  const int64_t n_units = p.n_tuples * Lyr * H;
+  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const int64_t t = u / (Lyr * H);
+    const int l = (int)((u / H) % Lyr), h = (int)(u % H);
+    const int L = p.seq_len[t];
+    if (L < 1 || L > kBuildMaxTokens) continue;  // documented limit (device data: skipped)
+    __syncthreads();
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+      s_mu[d] = p.mu[((size_t)l * H + h) * D + d];
+      s_s2[d] = p.sigma2[((size_t)l * H + h) * D + d];
+    }
+    __syncthreads();
+    const int64_t pbase = p.indptr[t];
+    auto src_row = [&](int which, int i) -> const uint16_t* {
+      const int64_t page = p.src_ids[pbase + i / 16];
+      return p.src_pool + (size_t)page * p.page_elems +
+             ((((size_t)l * 2 + which) * H + h) * 16 + i % 16) * D;
+    };
+    int N = 1;
+    while (N < L) N <<= 1;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      if (i < L) {
+        const uint16_t* k = src_row(0, i);
+        double a = 0.0, b = 0.0;
+        for (int d = 0; d < D; d += 8) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(k + d));
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const double x = bf16_to_double((uint16_t)(e & 1 ? w[e >> 1] >> 16 : w[e >> 1] & 0xFFFFu));
+            a = __dadd_rn(a, __dmul_rn((double)s_mu[d + e], x));
+            b = __dadd_rn(b, __dmul_rn((double)s_s2[d + e], __dmul_rn(x, x)));
+          }
+        }
+        key[i] = __dadd_rn(__dmul_rn(a, p.inv_sqrt_d), __dmul_rn(b, p.inv_2d));
+        idx[i] = i;
+      } else {
+        key[i] = -CUDART_INF;
+        idx[i] = 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    // bitonic sort: final order has precedes(i, i+1)
+    for (int k = 2; k <= N; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const bool up = (i & k) == 0;  // this pair must end in `precedes` order
+            const double ka = key[i], kb = key[ixj];
+            const int ia = idx[i], ib = idx[ixj];
+            const bool swap = up ? precedes(kb, ib, ka, ia) : precedes(ka, ia, kb, ib);
+            if (swap) {
+              key[i] = kb; key[ixj] = ka;
+              idx[i] = ib; idx[ixj] = ia;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    // gather: rank r ← token idx[r]; 16-byte chunks of the K and V rows
+    const int chunks = D / 8;
+    for (int w = threadIdx.x; w < L * 2 * chunks; w += blockDim.x) {
+      const int r = w / (2 * chunks), rem = w - r * 2 * chunks;
+      const int which = rem / chunks, ch = rem - which * chunks;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(src_row(which, idx[r]) + ch * 8));
+      const int64_t page = p.dst_ids[pbase + r / 16];
+      uint16_t* dst = p.dst_pool + (size_t)page * p.page_elems +
+                      ((((size_t)l * 2 + which) * H + h) * 16 + r % 16) * D + ch * 8;
+      *reinterpret_cast<uint4*>(dst) = v;
+    }
+  }
+}
+
+}  // namespace
+
+size_t build_smem_bytes(int head_dim) {
+  return (size_t)kBuildMaxTokens * (sizeof(double) + sizeof(int)) + 2 * sizeof(float) * head_dim;
+}
+
+cudaError_t launch_build(const BuildParams& p, cudaStream_t s) {
+  const size_t smem = build_smem_bytes(p.head_dim);
+  static bool attr = false;
+  if (!attr) {  // sized for the largest head_dim once
+    cudaFuncSetAttribute(build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)build_smem_bytes(128));
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t units = p.n_tuples * p.n_layers * p.n_kv_heads;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)sms * 4));
+  build_kernel<<<grid, kBuildThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ko

@@ -144,6 +144,23 @@ struct EmbedParams {
 };
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s);
 
+// importance-ordered cache builder (ko_build.cu)
+struct BuildParams {
+  const uint16_t* src_pool;
+  const int64_t* indptr;
+  const int32_t* src_ids;
+  const int32_t* seq_len;
+  int64_t n_tuples;
+  int32_t n_layers, n_kv_heads, head_dim;
+  int64_t page_elems;
+  const float* mu;      // [n_layers][n_kv_heads][head_dim]
+  const float* sigma2;  // same
+  uint16_t* dst_pool;
+  const int32_t* dst_ids;
+  double inv_sqrt_d, inv_2d;
+};
+cudaError_t launch_build(const BuildParams& p, cudaStream_t s);
+
 // soft relaxation of one plan (ko_soft.cu)
 struct SoftParams {
   ko_plan plan;
