@@ -133,6 +133,7 @@ struct Workspace {
   uint32_t* tuple_state;
   int32_t* worklist;
   int32_t* round_wl;              // [KO_MAX_STAGES][n_tuples] per-position worklists
+  ko_plan* gplans;                // [KO_MAX_PLANS] device copy of the plans
   uint32_t* tuple_done;           // [n_tuples]
   float* wm;                      // [n_ops][n_variants][n_tuples]
   int32_t* wc;
@@ -166,6 +167,7 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_va
   w.tuple_state = (uint32_t*)take(sizeof(uint32_t) * nt);
   w.worklist = (int32_t*)take(sizeof(int32_t) * nt);
   w.round_wl = (int32_t*)take(sizeof(int32_t) * nt * KO_MAX_STAGES);
+  w.gplans = (ko_plan*)take(sizeof(ko_plan) * KO_MAX_PLANS);
   w.tuple_done = (uint32_t*)take(sizeof(uint32_t) * nt);
   w.wm = (float*)take(sizeof(float) * nt * n_ops * n_variants);
   w.wc = (int32_t*)take(sizeof(int32_t) * nt * n_ops * n_variants);
@@ -399,6 +401,10 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     sp.gold = gold;
     sp.counts = (unsigned long long*)counts;
     for (int g = 0; g < n_plans; ++g) sp.plans[g] = plans[g];
+    sp.gplans = ws.gplans;
+    pp.gplans = ws.gplans;
+    pp.n_plans = n_plans;
+    for (int g = 0; g < n_plans; ++g) pp.plans[g] = plans[g];
     KO_CUDA(ko::launch_prep(pp, s));
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));

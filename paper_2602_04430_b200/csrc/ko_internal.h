@@ -56,6 +56,8 @@ struct ScoreParams {
   // prepared tensor-core fragments (workspace)
   const uint4* qfrag;  // [n_l*Hkv][KS][32]
   const uint4* wfrag;  // [n_l*Hkv][NT][KS][32]
+  const ko_plan* gplans;  // device copy of plans[] (lanes read different plans: L1, not the
+                          // constant bank, which serialises divergent reads)
   // scratch (workspace)
   float* part;                     // [n_work][n_l*Hkv][n_ops][n_var][CPR]
   int32_t* done;                   // [n_work]
@@ -99,6 +101,9 @@ struct PrepParams {
   int32_t op_classes[kMaxOps];
   uint4* qfrag;
   uint4* wfrag;
+  int32_t n_plans;
+  ko_plan* gplans;  // prep copies plans[] here (device)
+  ko_plan plans[kMaxPlans];
 };
 
 struct RouteParams {

@@ -521,22 +521,41 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     if (last) {
     __threadfence();
 
+    // z = b + Σ_u partial_u over the units whose layer is inside the variant's cut, for every
+    // (op, variant, class) entry: lane u loads unit u's partials (all entries issued at once, so
+    // the L2 latency is paid once, not once per unit), then a fixed xor-tree per entry — a fixed
+    // summation order, so margins stay bitwise reproducible.
     float* zs = s_z[warp];
     const int nz = p.n_ops * p.n_var * CPR;
-    for (int idx = lane; idx < nz; idx += 32) {
-      const int c = idx % CPR;
-      const int v = (idx / CPR) % p.n_var;
-      const int o = idx / (CPR * p.n_var);
-      float zf = -CUDART_INF_F;
-      if (c < p.op_classes[o]) {
-        double z = (double)__ldg(p.bias[o] + c);
-        const float* src = p.part + ((size_t)wslot * p.n_l * Hkv * p.n_ops + o) * p.n_var * CPR + v * CPR + c;
-        const size_t ustride = (size_t)p.n_ops * p.n_var * CPR;
-        const int u_end = min(p.cut[v], p.n_l) * Hkv;  // units are l-major: l < cut ⇔ u < cut·Hkv
-        for (int uu = 0; uu < u_end; ++uu) z += (double)__ldcg(src + uu * ustride);
-        zf = (float)z;
+    const int n_pu = p.n_l * Hkv;  // partial slots per tuple (layer-major)
+    const float* tpart = p.part + (size_t)wslot * n_pu * nz;
+    for (int e0 = 0; e0 < nz; e0 += 8) {
+      double acc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+      for (int u0 = 0; u0 < n_pu; u0 += 32) {
+        const int uu = u0 + lane;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int idx = e0 + k;
+          if (idx < nz && uu < n_pu) {
+            const int v = (idx / CPR) % p.n_var;
+            if (uu < min(p.cut[v], p.n_l) * Hkv)  // units are l-major: l < cut ⇔ u < cut·Hkv
+              acc[k] += (double)__ldcg(tpart + (size_t)uu * nz + idx);
+          }
+        }
       }
-      zs[idx] = zf;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+        const int idx = e0 + k;
+        if (lane == 0 && idx < nz) {
+          const int c = idx % CPR, o = idx / (CPR * p.n_var);
+          zs[idx] = c < p.op_classes[o] ? (float)((double)__ldg(p.bias[o] + c) + acc[k])
+                                        : -CUDART_INF_F;
+        }
+      }
     }
     __syncwarp();
     const bool walk = p.mode == MODE_WALK;
@@ -578,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     __syncwarp();
     if (p.mode == MODE_GRID) {
       for (int gp = lane; gp < p.n_plans; gp += 32)
-        eval_plan(p.plans[gp], s_m[warp], s_c[warp], p.n_var_total, p.op_classes_g, p.gold, p.n_tuples,
+        eval_plan(p.gplans[gp], s_m[warp], s_c[warp], p.n_var_total, p.op_classes_g, p.gold, p.n_tuples,
                   t, s_cnt + gp * kCountsPerPlan);
     } else if (walk && lane == 0) {
       // Routed execution: this launch is plan position `pos` = (operator group, variant rank).
@@ -664,6 +683,9 @@ __device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) {
 }
 
 __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
+  if (blockIdx.x == 0 && p.gplans)
+    for (int i = threadIdx.x; i < p.n_plans * (int)(sizeof(ko_plan) / 4); i += blockDim.x)
+      reinterpret_cast<uint32_t*>(p.gplans)[i] = reinterpret_cast<const uint32_t*>(p.plans)[i];
   const int KS = p.head_dim / 16;
   const int NT = p.nolo ? (p.CPR0 + 1) / 2 + (p.CPR1 + 1) / 2 : p.CPR0 + p.CPR1;
   const int Hq = p.n_kv_heads * p.gqa;
@@ -887,6 +909,9 @@ __global__ void final_counts_kernel(const __grid_constant__ RouteParams p) {
 // G-plan grid on precomputed margins: one warp per tuple, one lane per plan
 __global__ void reduce_kernel(const __grid_constant__ ReduceParams p) {
   __shared__ int s_cnt[kMaxPlans * kCountsPerPlan];
+  __shared__ ko_plan s_plans[kMaxPlans];  // lanes read different plans: smem, not the param bank
+  for (int i = threadIdx.x; i < p.n_plans * (int)(sizeof(ko_plan) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s_plans)[i] = reinterpret_cast<const uint32_t*>(p.plans)[i];
   __shared__ float s_m[8][kMaxOps * kMaxVar];
   __shared__ int32_t s_c[8][kMaxOps * kMaxVar];
   for (int i = threadIdx.x; i < p.n_plans * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
@@ -901,7 +926,7 @@ __global__ void reduce_kernel(const __grid_constant__ ReduceParams p) {
     }
     __syncwarp();
     for (int gp = lane; gp < p.n_plans; gp += 32)
-      eval_plan(p.plans[gp], s_m[w], s_c[w], p.n_variants, p.n_classes, p.gold, p.n_tuples, t,
+      eval_plan(s_plans[gp], s_m[w], s_c[w], p.n_variants, p.n_classes, p.gold, p.n_tuples, t,
                 s_cnt + gp * kCountsPerPlan);
     __syncwarp();
   }
