@@ -286,7 +286,7 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   sp.unit_counter = ws.unit_counter;
   sp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kv->head_dim));
   // Work-unit size: a unit streams HG kv-heads of one (tuple, layer) back-to-back, HG chosen so
-  // a unit is ~32 pages (estimated from the pool's average pages per tuple and the largest
+  // a unit is ~64 pages (estimated from the pool's average pages per tuple and the largest
   // keep‰), which hides the per-unit start-up latency behind the stream for short tuples.
   {
     int max_keep = 1;
@@ -298,8 +298,13 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
       const char* e = std::getenv("KO_HEADS_PER_UNIT");
       return e ? std::atoi(e) : 0;
     }();
+    static const double unit_pages = [] {  // tuning knob (A/B): target pages per work unit
+      const char* e = std::getenv("KO_UNIT_PAGES");
+      return e ? std::atof(e) : 64.0;
+    }();
     int hg = 1;
-    while (hg * 2 <= kv->n_kv_heads && kv->n_kv_heads % (hg * 2) == 0 && (hg * 2) * ppu <= 32.0)
+    while (hg * 2 <= kv->n_kv_heads && kv->n_kv_heads % (hg * 2) == 0 &&
+           (hg * 2) * ppu <= unit_pages)
       hg *= 2;
     if (hg_env > 0 && kv->n_kv_heads % hg_env == 0) hg = hg_env;
     sp.heads_per_unit = hg;
