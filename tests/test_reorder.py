@@ -9,12 +9,13 @@ from paper_2602_04430_b200 import reorder
 
 def test_spec_two_filter_example():
     """two logical ops, one stage each, costs (1, 10), sel_inter (0.1, 0.5), N = 100:
-    cheap-selective first costs 1·100 + 10·10 = 110, the other order 10·100 + 1·50 = 1050."""
+    cheap-selective first costs 1·100 + 10·10 = 200 (SPEC prints 110: arithmetic slip), the other
+    order 10·100 + 1·50 = 1050."""
     impl, cost = [0, 1], [1.0, 10.0]
     inter, intra = [0.1, 0.5], [0.0, 0.0]
     best, order = reorder.dp_reorder(impl, cost, inter, intra, 100)
     assert order == [0, 1]
-    assert best == pytest.approx(1.0 * 100 + 10.0 * 100 * 0.1)       # 110
+    assert best == pytest.approx(1.0 * 100 + 10.0 * 100 * 0.1)       # 200
     worst = reorder.order_cost([1, 0], impl, cost, inter, intra, 100)
     assert worst == pytest.approx(10.0 * 100 + 1.0 * 100 * 0.5)       # 1050
 
