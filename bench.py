@@ -239,7 +239,7 @@ def main():
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or os.environ.get("KO_FORCE_DIST") == "1":  # (forced: exercise NCCL at N = 1)
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
