@@ -278,7 +278,7 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   // bf16 readouts of a multi-class tile: two classes per W·V tile (no lo residual)
   bool all_bf16 = true;
   for (int i = 0; i < n_sel; ++i) all_bf16 = all_bf16 && ops[op_sel[i]].w_is_bf16;
-  pp.nolo = all_bf16 && *CPR0 >= 2 && *CPR1 == 0;
+  pp.nolo = all_bf16 && *CPR0 >= 2 && *CPR1 <= 1;
   sp.qfrag = ws.qfrag;
   sp.wfrag = ws.wfrag;
   sp.part = ws.part;
@@ -453,13 +453,17 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   for (int i = 0; i < P.n_stages; ++i) {
     const int o = P.stage[i].op;
     if (group_of_op[o] >= 0) continue;
+    static const int fuse_maps = [] {  // tuning knob (A/B): bf16 maps join the filter tile
+      const char* e = std::getenv("KO_FUSE_MAPS");
+      return e ? std::atoi(e) : 0;
+    }();
+    const bool joinable = ops[o].n_classes <= 1 || (fuse_maps && ops[o].w_is_bf16);
     int g;
-    if (ops[o].n_classes <= 1 && filter_group >= 0 &&
-        (group_n[filter_group] + 1) * rows_per_op <= KO_MAX_ROWS) {
+    if (joinable && filter_group >= 0 && (group_n[filter_group] + 1) * rows_per_op <= KO_MAX_ROWS) {
       g = filter_group;
     } else {
       g = n_groups++;
-      if (ops[o].n_classes <= 1) filter_group = g;
+      if (joinable) filter_group = g;
     }
     group_of_op[o] = g;
     group_ops[g][group_n[g]++] = o;

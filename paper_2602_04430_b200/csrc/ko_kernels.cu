@@ -1074,15 +1074,16 @@ cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1,
 #define KO_DISPATCH(DD, C0, C1)                                                       \
   if (head_dim == DD && CPR0 == C0 && CPR1 == C1 && !nolo)                           \
     return launch_score_t<DD, C0, C1, false>(p, max_units, s);
-#define KO_DISPATCH_NOLO(DD, C0)                                                      \
-  if (head_dim == DD && CPR0 == C0 && CPR1 == 0 && nolo)                             \
-    return launch_score_t<DD, C0, 0, true>(p, max_units, s);
+#define KO_DISPATCH_NOLO(DD, C0, C1)                                                  \
+  if (head_dim == DD && CPR0 == C0 && CPR1 == C1 && nolo)                            \
+    return launch_score_t<DD, C0, C1, true>(p, max_units, s);
 #define KO_DISPATCH_D(DD)                                                                  \
   KO_DISPATCH(DD, 1, 0) KO_DISPATCH(DD, 1, 1) KO_DISPATCH(DD, 2, 0) KO_DISPATCH(DD, 2, 1)   \
   KO_DISPATCH(DD, 2, 2) KO_DISPATCH(DD, 4, 0) KO_DISPATCH(DD, 4, 1) KO_DISPATCH(DD, 4, 2)   \
   KO_DISPATCH(DD, 4, 4) KO_DISPATCH(DD, 8, 0) KO_DISPATCH(DD, 8, 1) KO_DISPATCH(DD, 8, 2)   \
   KO_DISPATCH(DD, 8, 4) KO_DISPATCH(DD, 8, 8)                                              \
-  KO_DISPATCH_NOLO(DD, 2) KO_DISPATCH_NOLO(DD, 4) KO_DISPATCH_NOLO(DD, 8)
+  KO_DISPATCH_NOLO(DD, 2, 0) KO_DISPATCH_NOLO(DD, 4, 0) KO_DISPATCH_NOLO(DD, 8, 0)          \
+  KO_DISPATCH_NOLO(DD, 2, 1) KO_DISPATCH_NOLO(DD, 4, 1) KO_DISPATCH_NOLO(DD, 8, 1)
   KO_DISPATCH_D(64)
   KO_DISPATCH_D(128)
 #undef KO_DISPATCH_D
