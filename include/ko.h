@@ -168,7 +168,8 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
  *                tuples that reach stage s+1 (none when s is the last stage).
  * tuple_state: device uint32 [n_tuples] in/out.  bit 0 = alive; bits 1+2o..2+2o = status of op o
  *              (0 pending, 1 accepted/resolved, 2 rejected); bits 16+4o..19+4o = resolved class
- *              of map op o.  Initialise to 1 (alive, all pending) before stage 0.
+ *              of map op o; bits 9..15 are reserved (the score_batch routed executor keeps its
+ *              resume stage there).  Initialise to 1 (alive, all pending) before stage 0.
  * worklist_out: device int32 [n_tuples]; worklist_len: device int64 scalar (overwritten).  The
  *              order of the worklist is unspecified (compare as a set).                      */
 ko_status ko_route(const ko_plan* plan, const float* margins, const int32_t* classes,

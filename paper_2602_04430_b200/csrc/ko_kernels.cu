@@ -68,6 +68,9 @@ __device__ __forceinline__ int decide(float m, const ko_stage& st, int ncls) {
 }
 
 __device__ __forceinline__ int op_status(uint32_t st, int o) { return (st >> (1 + 2 * o)) & 3; }
+// routed walk: the stage a tuple resumes at lives in the free bits 9..12 (bits 1..8 hold the
+// op statuses, 16..31 the resolved classes of ops 0..3)
+constexpr int kWalkStageShift = 9;
 
 // Whole-plan evaluation for one tuple (Eqs. accept-i/reject-i/unsure-i, conjunctive
 // inter-op semantics P:536-539, counts P:350-352).  ms/cs: margins/classes indexed
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         const uint32_t mine = (uint32_t)p.round + 1u;
         if (cur == 15u || cur < mine) done = (done & ~(15u << (4 * p.group))) | (mine << (4 * p.group));
       }
-      int s = (int)((state >> 24) & 15u);
+      int s = (int)((state >> kWalkStageShift) & 15u);
       for (; s < P.n_stages; ++s) {
         const ko_stage& st = P.stage[s];
         const int o = st.op;
@@ -662,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
           atomicAdd(&cnt[3], 1);
         }
       }
-      p.tuple_state[t] = (state & ~(15u << 24)) | ((uint32_t)s << 24);
+      p.tuple_state[t] = (state & ~(15u << kWalkStageShift)) | ((uint32_t)s << kWalkStageShift);
       p.tuple_done[t] = done;
     }
     }  // last
