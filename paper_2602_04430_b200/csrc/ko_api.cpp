@@ -137,12 +137,15 @@ struct Workspace {
   uint32_t* tuple_done;           // [n_tuples]
   float* wm;                      // [n_ops][n_variants][n_tuples]
   int32_t* wc;
+  float* rstate;                  // [n_ops groups][n_tuples][n_layers][Hkv][8][rstate_w]
+  int rstate_w;
+  size_t rstate_group;            // floats per group slice
   size_t total;
 };
 
 // Layout: [counters 256 B][done][part][qfrag][wfrag][tuple_state][worklist][position
 // worklists][tuple_done][wm][wc]
-Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_variants,
+Workspace layout(const ko_kv_cache* kv, int max_cls, int max_ent, int32_t n_ops, int32_t n_variants,
                  int64_t n_work, uint8_t* base) {
   Workspace w{};
   const int CPR = pow2_at_least(max_cls);
@@ -160,8 +163,9 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_va
   w.worklist_len = ctr ? (unsigned long long*)(ctr + 8) : nullptr;
   w.round_len = ctr ? (unsigned long long*)(ctr + 64) : nullptr;
   w.done = (int32_t*)take(sizeof(int32_t) * (size_t)std::max<int64_t>(n_work, 1));
-  w.part = (float*)take(sizeof(float) * (size_t)std::max<int64_t>(n_work, 1) * kv->n_layers *
-                        kv->n_kv_heads * n_ops * n_variants * CPR);
+  // partials: per work slot (grid) or per tuple (walk: they persist across the rounds of a call)
+  w.part = (float*)take(sizeof(float) * (size_t)std::max<int64_t>(std::max<int64_t>(n_work, kv->n_tuples), 1) *
+                        kv->n_layers * kv->n_kv_heads * n_ops * n_variants * CPR);
   w.qfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * KS * 32);
   w.wfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * NT * KS * 32);
   w.tuple_state = (uint32_t*)take(sizeof(uint32_t) * nt);
@@ -171,6 +175,11 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_va
   w.tuple_done = (uint32_t*)take(sizeof(uint32_t) * nt);
   w.wm = (float*)take(sizeof(float) * nt * n_ops * n_variants);
   w.wc = (int32_t*)take(sizeof(int32_t) * nt * n_ops * n_variants);
+  // saved softmax states of the routed rounds: a group's table needs ≤ pow2(max entries per row)
+  // tiles, so 4 + 2·that floats per lane group bound every group's state
+  w.rstate_w = 4 + 2 * std::min(ko::kMaxTNT, pow2_at_least(std::max(max_ent, 1)));
+  w.rstate_group = nt * kv->n_layers * kv->n_kv_heads * 8 * (size_t)w.rstate_w;
+  w.rstate = (float*)take(sizeof(float) * w.rstate_group * n_ops);
   w.total = off;
   return w;
 }
@@ -178,6 +187,12 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int32_t n_ops, int32_t n_va
 int max_classes(const ko_operator* ops, int n_ops) {
   int m = 1;
   for (int o = 0; o < n_ops; ++o) m = std::max(m, (int)ops[o].n_classes);
+  return m;
+}
+// W·V entries of one row of the table packing: classes, ×2 for fp32 readouts (hi + lo)
+int max_entries(const ko_operator* ops, int n_ops) {
+  int m = 1;
+  for (int o = 0; o < n_ops; ++o) m = std::max(m, (int)ops[o].n_classes * (ops[o].w_is_bf16 ? 1 : 2));
   return m;
 }
 
@@ -216,10 +231,60 @@ ko_status make_tmap(CUtensorMap* map, const ko_kv_cache* kv) {
 // (caller indices op_sel[0..n_sel)) and variants.  Row slots: the selected ops are laid out in
 // descending class count, n_q·gqa rows each, slot = half·8 + g; CPR0 / CPR1 (returned) are the
 // power-of-two class counts of the two halves of the 16-row tile (CPR1 = 0: one half used).
+// Table packing (walk mode): every S row (op, gqa member, query row) of the selected ops goes to
+// one of 8 lane groups holding ≤ 2 rows (S rows g and g + 8); a row of a C-class op needs C W·V
+// entries (2C for fp32 W: bf16 hi and lo), and a lane group's entries fill the 2·NT slots of NT
+// tiles.  Smallest supported NT by first-fit decreasing; 0 if none ≤ kMaxTNT fits.
+int pack_table(const ko_operator* ops, const int* order, int n_sel, int rows_per_op,
+               ko::ScoreParams& sp, ko::PrepParams& pp) {
+  struct Row { int i, rem, e; };
+  Row rows[16];
+  int nr = 0;
+  for (int i = 0; i < n_sel; ++i)
+    for (int r = 0; r < rows_per_op; ++r) {
+      if (nr == 16) return 0;
+      rows[nr++] = {i, r, (int)ops[order[i]].n_classes * (ops[order[i]].w_is_bf16 ? 1 : 2)};
+    }
+  std::stable_sort(rows, rows + nr, [](const Row& a, const Row& b) { return a.e > b.e; });
+  for (int NT : {1, 2, 4, 8}) {
+    int bin_n[8] = {0}, bin_e[8] = {0}, bin_row[8][2];
+    bool ok = true;
+    for (int k = 0; k < nr && ok; ++k) {
+      int b = 0;
+      while (b < 8 && !(bin_n[b] < 2 && bin_e[b] + rows[k].e <= 2 * NT)) ++b;
+      if (b == 8) { ok = false; break; }
+      bin_row[b][bin_n[b]++] = k;
+      bin_e[b] += rows[k].e;
+    }
+    if (!ok) continue;
+    for (int r = 0; r < 16; ++r) { sp.slot_op[r] = -1; pp.slot_op[r] = -1; pp.slot_rem[r] = 0; }
+    for (int b = 0; b < 8; ++b) {
+      sp.tbl_sel[b] = 0;
+      for (int k = 0; k < 16; ++k) { sp.tbl_tgt[b][k] = -1; pp.tbl_w[b][k] = -1; }
+      int k = 0;
+      for (int hs = 0; hs < bin_n[b]; ++hs) {
+        const Row& R = rows[bin_row[b][hs]];
+        sp.slot_op[hs * 8 + b] = R.i;
+        pp.slot_op[hs * 8 + b] = R.i;
+        pp.slot_rem[hs * 8 + b] = R.rem;
+        const ko_operator& op = ops[order[R.i]];
+        for (int c = 0; c < op.n_classes; ++c)
+          for (int lo = 0; lo < (op.w_is_bf16 ? 1 : 2); ++lo, ++k) {
+            pp.tbl_w[b][k] = R.i | (R.rem << 3) | (c << 8) | (lo << 12);
+            sp.tbl_tgt[b][k] = (int8_t)(R.i * 8 + c);
+            if (hs) sp.tbl_sel[b] |= 1u << k;
+          }
+      }
+    }
+    return NT;
+  }
+  return 0;
+}
+
 void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
                  const ko_operator* ops, const int* op_sel, int n_sel, const ko_variant* variants,
                  const int* var_sel, int n_vsel, int32_t n_ops_total, int32_t n_var_total,
-                 const Workspace& ws, int* CPR0, int* CPR1) {
+                 const Workspace& ws, int* CPR0, int* CPR1, int* TNT = nullptr) {
   std::memset(&sp, 0, sizeof(sp));
   std::memset(&pp, 0, sizeof(pp));
   sp.pool = (const uint16_t*)kv->kv_pool;
@@ -279,6 +344,16 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   bool all_bf16 = true;
   for (int i = 0; i < n_sel; ++i) all_bf16 = all_bf16 && ops[op_sel[i]].w_is_bf16;
   pp.nolo = all_bf16 && *CPR0 >= 2 && *CPR1 <= 1;
+  pp.tbl_nt = 0;
+  if (TNT) {  // table packing replaces the half/class layout above
+    *TNT = pack_table(ops, order, n_sel, sp.rows_per_op, sp, pp);
+    *CPR0 = pow2_at_least(std::max(half_cls[0], half_cls[1]));
+    *CPR1 = 0;
+    pp.nolo = 0;
+    pp.tbl_nt = *TNT;
+    pp.CPR0 = *CPR0;
+    pp.CPR1 = 0;
+  }
   sp.qfrag = ws.qfrag;
   sp.wfrag = ws.wfrag;
   sp.part = ws.part;
@@ -317,8 +392,10 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   pp.head_dim = kv->head_dim;
   pp.n_ops = n_sel;
   pp.rows_per_op = sp.rows_per_op;
-  pp.CPR0 = *CPR0;
-  pp.CPR1 = *CPR1;
+  if (!TNT) {
+    pp.CPR0 = *CPR0;
+    pp.CPR1 = *CPR1;
+  }
   pp.qfrag = ws.qfrag;
   pp.wfrag = ws.wfrag;
 }
@@ -340,7 +417,8 @@ size_t ko_workspace_size(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
                          int32_t n_variants, int64_t n_work) {
   if (validate_kv(kv) != KO_OK || validate_ops(kv, ops, n_ops) != KO_OK) return 0;
   if (n_variants < 1 || n_variants > KO_MAX_VARIANTS || n_work < 0) return 0;
-  return layout(kv, max_classes(ops, n_ops), n_ops, n_variants, n_work, nullptr).total;
+  return layout(kv, max_classes(ops, n_ops), max_entries(ops, n_ops), n_ops, n_variants, n_work,
+                nullptr).total;
 }
 
 ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t n_ops,
@@ -374,7 +452,8 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
                 n_ops * kv->gqa_group * kv->n_q, KO_MAX_ROWS);
   if (!workspace) return fail(KO_EINVAL, "workspace is NULL");
   if (((uintptr_t)workspace & 255) != 0) return fail(KO_EINVAL, "workspace not 256-byte aligned");
-  Workspace ws = layout(kv, maxc, n_ops, n_variants, n_work, (uint8_t*)workspace);
+  Workspace ws = layout(kv, maxc, max_entries(ops, n_ops), n_ops, n_variants, n_work,
+                        (uint8_t*)workspace);
   if (workspace_bytes < ws.total)
     return fail(KO_EWORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, ws.total);
   cudaStream_t s = (cudaStream_t)stream;
@@ -414,7 +493,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0,
+    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0, 0,
                              n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end) KO_CUDA(cudaEventRecord(g_trace_end, s));
     return KO_OK;
@@ -443,31 +522,49 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   rp.gold = gold;
   rp.counts = (unsigned long long*)counts;
 
-  // Operator groups: the referenced filters fused into row tiles of ≤ 16 rows, each map alone
-  // (a K-class map needs K readout tiles).  Variant ranks: the plan's distinct variants ordered
-  // by extent (keep‰ · layers); a launch of rank r computes every variant of rank ≤ r in one read.
+  // Operator groups: the referenced ops fused into ONE read while their rows fit one 16-row tile
+  // and the table packing stays within 4 W·V tiles (a speculative op costs tensor-core work on
+  // bytes the read moves anyway, never extra bytes); otherwise a new group starts.  KO_FUSE=0
+  // (A/B knob): only filters are fused, each map is a group of its own.
   const int rows_per_op = kv->gqa_group * kv->n_q;
+  static const int fuse_all = [] {
+    const char* e = std::getenv("KO_FUSE");
+    return e ? std::atoi(e) : 1;
+  }();
   int group_of_op[KO_MAX_OPS] = {-1, -1, -1, -1};
   int group_ops[KO_MAX_OPS][KO_MAX_OPS], group_n[KO_MAX_OPS] = {0, 0, 0, 0}, n_groups = 0;
-  int filter_group = -1;
+  auto packs = [&](const int* sel, int n) {
+    if (n * rows_per_op > KO_MAX_ROWS) return false;
+    ko::ScoreParams tsp;
+    ko::PrepParams tpp;
+    const int nt = pack_table(ops, sel, n, rows_per_op, tsp, tpp);
+    return nt > 0 && nt <= 4;
+  };
   for (int i = 0; i < P.n_stages; ++i) {
     const int o = P.stage[i].op;
     if (group_of_op[o] >= 0) continue;
-    static const int fuse_maps = [] {  // tuning knob (A/B): bf16 maps join the filter tile
-      const char* e = std::getenv("KO_FUSE_MAPS");
-      return e ? std::atoi(e) : 0;
-    }();
-    const bool joinable = ops[o].n_classes <= 1 || (fuse_maps && ops[o].w_is_bf16);
-    int g;
-    if (joinable && filter_group >= 0 && (group_n[filter_group] + 1) * rows_per_op <= KO_MAX_ROWS) {
-      g = filter_group;
-    } else {
+    int g = -1;
+    for (int c = n_groups - 1; c >= 0 && g < 0; --c) {
+      const bool maps_alone = !fuse_all && (ops[o].n_classes > 1 || ops[group_ops[c][0]].n_classes > 1);
+      if (maps_alone) continue;
+      int sel[KO_MAX_OPS];
+      for (int k = 0; k < group_n[c]; ++k) sel[k] = group_ops[c][k];
+      sel[group_n[c]] = o;
+      if (packs(sel, group_n[c] + 1)) g = c;
+    }
+    if (g < 0) {
       g = n_groups++;
-      if (joinable) filter_group = g;
+      if (!packs(&o, 1))
+        return fail(KO_EUNSUPPORTED, "routed mode: op %d needs more than 4 W·V tiles (%d classes, %s W)",
+                    o, ops[o].n_classes, ops[o].w_is_bf16 ? "bf16" : "fp32");
     }
     group_of_op[o] = g;
     group_ops[g][group_n[g]++] = o;
   }
+  // Variant ranks: the plan's distinct KV variants ordered by extent (keep‰ · layers); a launch of
+  // round r streams the extents of ranks ≤ r.  A variant's margin is complete (available) after
+  // the first round r at which, for every layer l < its cut, some variant of rank ≤ r with cut > l
+  // keeps at least as many tokens — then every snapshot it needs was taken by a round ≤ r.
   int pv[KO_MAX_VARIANTS], n_pv = 0;
   bool seen_v[KO_MAX_VARIANTS] = {false};
   for (int i = 0; i < P.n_stages; ++i)
@@ -480,36 +577,76 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     const int64_t eb = (int64_t)variants[b].keep_permille * variants[b].layer_cut;
     return ea < eb;
   });
-  int var_rank[KO_MAX_VARIANTS];
+  int avail[KO_MAX_VARIANTS];
+  for (int k = 0; k < n_pv; ++k) {
+    const ko_variant& v = variants[pv[k]];
+    avail[k] = k;
+    for (int r = 0; r <= k; ++r) {
+      bool ok = true;
+      for (int l = 0; l < v.layer_cut && ok; ++l) {
+        bool cov = false;
+        for (int u = 0; u <= r && !cov; ++u)
+          cov = variants[pv[u]].layer_cut > l && variants[pv[u]].keep_permille >= v.keep_permille;
+        ok = cov;
+      }
+      if (ok) { avail[k] = r; break; }
+    }
+  }
+  int var_rank[KO_MAX_VARIANTS];  // caller's variant → round after which its margin is available
   for (int v = 0; v < KO_MAX_VARIANTS; ++v) var_rank[v] = (v < n_variants && is_external(variants[v])) ? -1 : 0;
-  for (int k = 0; k < n_pv; ++k) var_rank[pv[k]] = k;
+  for (int k = 0; k < n_pv; ++k) var_rank[pv[k]] = avail[k];
   if (!margins) {
     for (int i = 0; i < P.n_stages; ++i)
       if (is_external(variants[P.stage[i].variant]))
         return fail(KO_EINVAL, "routed plan uses an external variant but margins is NULL");
   }
+  int pos_group[KO_MAX_STAGES], pos_round[KO_MAX_STAGES];
+  for (int q = 0; q < P.n_stages; ++q) {
+    pos_group[q] = group_of_op[P.stage[q].op];
+    pos_round[q] = var_rank[P.stage[q].variant];
+  }
 
   // One launch per plan position (= stage): tuples are queued by their own plan walk to the
   // first later position that computes what they need, so one pass in plan order suffices.
+  // A position whose (group, round) is covered by position 0 never receives a tuple (position 0
+  // processes every tuple), so it is not launched.
   KO_CUDA(cudaMemsetAsync(ws.round_len, 0, sizeof(unsigned long long) * KO_MAX_STAGES, s));
+  int last_launch = 0;
+  for (int pos = 0; pos < P.n_stages; ++pos)
+    if (pos == 0 || !(pos_group[pos] == pos_group[0] && std::max(pos_round[pos], 0) <= std::max(pos_round[0], 0)))
+      last_launch = pos;
   for (int pos = 0; pos < P.n_stages; ++pos) {
-    const int g = group_of_op[P.stage[pos].op];
+    const int g = pos_group[pos];
     // a stage on an external variant computes nothing itself; its launch still walks the
-    // tuples queued there (with rank 0 extents, never needed by them)
-    const int r = std::max(var_rank[P.stage[pos].variant], 0);
-    int CPR0 = 1, CPR1 = 0;
+    // tuples queued there (with round 0 extents, never needed by them)
+    const int r = std::max(pos_round[pos], 0);
+    if (pos > 0 && g == pos_group[0] && r <= std::max(pos_round[0], 0)) continue;
+    int CPR0 = 1, CPR1 = 0, TNT = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
-    fill_common(sp, pp, kv, ops, group_ops[g], group_n[g], variants, pv, r + 1, n_ops, n_variants,
-                ws, &CPR0, &CPR1);
+    fill_common(sp, pp, kv, ops, group_ops[g], group_n[g], variants, pv, n_pv, n_ops, n_variants,
+                ws, &CPR0, &CPR1, &TNT);
+    if (TNT <= 0) return fail(KO_EUNSUPPORTED, "routed mode: table packing failed");
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
+    int n_l = 1;
+    for (int k = 0; k <= r && k < n_pv; ++k) n_l = std::max(n_l, (int)variants[pv[k]].layer_cut);
+    sp.n_l = n_l;
+    sp.n_lh_all = kv->n_layers * kv->n_kv_heads;
+    sp.avail_mask = 0;
+    for (int k = 0; k < n_pv; ++k)
+      if (avail[k] <= r) sp.avail_mask |= 1 << k;
+    sp.save_state = 0;
+    for (int q = 0; q < P.n_stages; ++q)
+      if (pos_group[q] == g && pos_round[q] > r) sp.save_state = 1;
+    sp.rstate = ws.rstate + (size_t)g * ws.rstate_group;
+    sp.rstate_w = ws.rstate_w;
     sp.pos = pos;
     sp.n_pos = P.n_stages;
     sp.group = g;
     sp.round = r;
     for (int q = 0; q < P.n_stages; ++q) {
-      sp.pos_group[q] = group_of_op[P.stage[q].op];
-      sp.pos_round[q] = var_rank[P.stage[q].variant];
+      sp.pos_group[q] = pos_group[q];
+      sp.pos_round[q] = pos_round[q];
       sp.wl[q] = ws.round_wl + (size_t)q * std::max<int64_t>(kv->n_tuples, 1);
       sp.wl_len[q] = ws.round_len + q;
     }
@@ -538,9 +675,9 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin && pos == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0,
+    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, false, TNT,
                              n_work * sp.n_l * kv->n_kv_heads, s));
-    if (g_trace_end && pos + 1 == P.n_stages) KO_CUDA(cudaEventRecord(g_trace_end, s));
+    if (g_trace_end && pos == last_launch) KO_CUDA(cudaEventRecord(g_trace_end, s));
   }
   KO_CUDA(ko::launch_final_counts(rp, s));
   return KO_OK;

@@ -17,6 +17,7 @@ constexpr int kMaxCls = KO_MAX_CLASSES;
 constexpr int kMaxPlans = KO_MAX_PLANS;
 constexpr int kCountsPerPlan = KO_COUNTS_PER_PLAN;
 constexpr int kThreads = 128;  // score kernel CTA size (4 warps, one work unit per warp)
+constexpr int kMaxTNT = 8;     // W·V tiles of the table-packed kernel (2·kMaxTNT slots per lane)
 
 enum Mode : int32_t { MODE_GRID = 0, MODE_STAGE = 1, MODE_WALK = 2 };
 
@@ -86,6 +87,21 @@ struct ScoreParams {
   uint32_t* tuple_done;          // per tuple: 4-bit (rank + 1) computed per group, 15 = none
   float* wm;                     // computed margins [n_ops][n_variants][n_tuples]
   int32_t* wc;                   // computed classes
+  // walk mode, resumable extents: local variants are ALL the plan's KV variants in rank order
+  // (local index = rank); this launch streams, per (tuple, layer), the tokens between the
+  // extent of the tuple's previous rank for this group and the extent of rank `round`, resuming
+  // the saved softmax state; partials persist per tuple; avail_mask = local variants whose
+  // margins are complete after this round.
+  int32_t avail_mask;
+  int32_t save_state;            // a later rank of this group exists: save the state at the end
+  float* rstate;                 // [n_tuples][n_layers][Hkv][8][rstate_w] (this group's slice)
+  int32_t rstate_w;              // floats per lane group: M[2], den[2], acc[2·NT]
+  int32_t n_lh_all;              // n_layers · Hkv (partials of walk mode are per tuple, all layers)
+  // table-driven row/class packing (template TNT > 0): per lane group g, W·V slot k = 2·tile +
+  // (A-row half) accumulates into S row g (sel bit 0) or g + 8 (sel bit 1) for local
+  // (op, class) tgt = op·8 + class (−1: unused)
+  uint32_t tbl_sel[8];
+  int8_t tbl_tgt[8][16];
   ko_plan plans[kMaxPlans];
 };
 
@@ -98,6 +114,10 @@ struct PrepParams {
   const float* w[kMaxOps];          // fp32 readout, or NULL when w_bf16 is given
   const uint16_t* w_bf16[kMaxOps];  // bf16 readout (ko_operator.w_is_bf16)
   int32_t nolo;                     // all ops bf16: two classes per W·V tile, no lo part
+  // table packing (tbl_nt > 0): W entry of lane group g, slot k = 2·tile + A-row half:
+  // −1 unused, else (local op) | rem << 3 | class << 8 | lo << 12 (lo: the fp32 residual part)
+  int32_t tbl_nt;
+  int32_t tbl_w[8][16];
   int32_t op_classes[kMaxOps];
   uint4* qfrag;
   uint4* wfrag;
@@ -183,8 +203,9 @@ cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s);
 
 // launchers (ko_kernels.cu); return cudaSuccess or the launch error
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
+// tnt > 0: table-packed kernel with tnt W·V tiles (CPR0 = class stride of the partials)
 cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, bool nolo,
-                         int64_t max_units, cudaStream_t s);
+                         int tnt, int64_t max_units, cudaStream_t s);
 cudaError_t launch_route_reach(const RouteParams& p, cudaStream_t s);  // build worklist for stage
 cudaError_t launch_route_apply(const RouteParams& p, cudaStream_t s);  // apply stage on margins
 cudaError_t launch_route_plan(const RouteParams& p, cudaStream_t s);   // whole plan on margins

@@ -197,14 +197,20 @@ struct Ring {
 //     tile(h, c) = h ? CPR0 + c : c, u = C[e] + C[2+e];
 //   bf16 W (NOLO = true, exact: no lo part): two classes per tile, class c in rows 0-7 (c even)
 //     or 8-15 (c odd): tile(h, c) = (h ? ⌈CPR0/2⌉ : 0) + c/2, u = C[2(c&1) + e].
-template <int D, int CPR0, int CPR1, bool NOLO>
+// TNT > 0 (table packing, every walk-mode launch): the W·V tiles are packed per lane group g
+// from a host table — A-row half hr of tile tt at lane group g is slot k = 2·tt + hr, which
+// accumulates into S row g (sel bit 0) or g + 8 (sel bit 1) for the (op, class) tgt[k] — so a
+// K-class map row and two filter rows share TNT = ⌈entries / 2⌉ tiles.
+template <int D, int CPR0, int CPR1, bool NOLO, int TNT>
 __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_constant__ ScoreParams p) {
+  constexpr bool TBL = TNT > 0;
   constexpr int KS = D / 16;  // mma k-steps over head_dim
   constexpr int KP = D / 32;  // 128-bit fragment reads per token row per lane (2 k-steps each)
-  constexpr int NH = CPR1 > 0 ? 2 : 1;
+  constexpr int NH = TBL ? 2 : (CPR1 > 0 ? 2 : 1);
   constexpr int CPR = CPR0;
   constexpr int T0 = NOLO ? (CPR0 + 1) / 2 : CPR0;  // tiles of half 0
-  constexpr int NT = NOLO ? T0 + (CPR1 + 1) / 2 : CPR0 + CPR1;
+  constexpr int NT = TBL ? TNT : (NOLO ? T0 + (CPR1 + 1) / 2 : CPR0 + CPR1);
+  constexpr int NSL = TBL ? 2 * TNT : 1;            // table slots per lane
   constexpr int WREG = NT <= 2 ? NT : 0;            // W·V tiles whose fragments stay in registers
   constexpr int S = Ring<D>::kStages;
   constexpr int STAGE = Ring<D>::kStageBytes;
@@ -224,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   uint8_t* ring = ring_base + warp * Ring<D>::kWarpBytes;
   const uint32_t ring_s = smem_u32(ring);
 
+  const bool walk = p.mode == MODE_WALK;
   const int n_cnt_rows = p.mode == MODE_GRID ? p.n_plans : (p.tuple_state ? 1 : 0);  // stage/walk: row 0
   for (int i = threadIdx.x; i < n_cnt_rows * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
   if (lane == 0) {
@@ -241,13 +248,33 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   const int HG = p.heads_per_unit;  // kv-heads streamed back-to-back by one unit (same pages)
   const int upt = p.n_l * (Hkv / HG);  // work units per tuple: (layer, group of HG kv-heads)
   const int64_t n_units = n_work * upt;
-  const int R = p.n_ops * p.rows_per_op;
+  // variants whose extents this launch streams: grid = all; walk = ranks ≤ round
+  const int v_hi = walk ? p.round : p.n_var - 1;
 
-  // row slot → local op for this lane's two half-slots
+  // row slot → local op for this lane's two half-slots (legacy packing)
   int slot_op[NH];
 #pragma unroll
   for (int hs = 0; hs < NH; ++hs) slot_op[hs] = p.slot_op[hs * 8 + g];
-  (void)R;
+  // table packing: this lane group's slot → S-row half (bit k) and target (op·8 + class)
+  uint32_t tsel = 0;
+  int tgt[NSL];
+#pragma unroll
+  for (int k = 0; k < NSL; ++k) tgt[k] = -1;
+  // snapshot reduction: lane j owns target j = op·8 + class; red0/red1 = its slots' positions
+  // g·NSL + k (bits 0-63 / 64-127)
+  uint64_t red0 = 0, red1 = 0;
+  if constexpr (TBL) {
+    tsel = p.tbl_sel[g];
+#pragma unroll
+    for (int k = 0; k < NSL; ++k) tgt[k] = p.tbl_tgt[g][k];
+    for (int gg = 0; gg < 8; ++gg)
+#pragma unroll
+      for (int k = 0; k < NSL; ++k)
+        if (p.tbl_tgt[gg][k] == lane) {
+          const int i = gg * NSL + k;
+          if (i < 64) red0 |= 1ull << i; else red1 |= 1ull << (i - 64);
+        }
+  }
 
   // lane-constant smem offsets of this lane's fragment reads inside a stage: token row g (+8),
   // d-chunk (2q + (j & 1)) of box (j >> 1), XOR-swizzled by the row (= token mod 8)
@@ -269,28 +296,56 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     const int64_t t = p.work ? (int64_t)p.work[wslot] : wslot;
     const int L = p.seq_len[t];
 
-    // tokens this unit must stream: the largest prefix among variants whose cut includes l
-    int n_need = 0;
-    for (int v = 0; v < p.n_var; ++v)
-      if (p.cut[v] > l) n_need = max(n_need, n_kept(L, p.keep[v]));
-    int first_snap = n_need;  // smallest active n_kept (first snapshot point)
-    for (int v = 0; v < p.n_var; ++v)
-      if (p.cut[v] > l) first_snap = min(first_snap, n_kept(L, p.keep[v]));
+    // tokens [s0, s1) this unit streams: s1 = the largest prefix among the streamed variants whose
+    // cut includes l; walk mode resumes after the extent of the tuple's previous rank (s0)
+    int prev = -1;
+    if (walk && p.pos > 0) {
+      const uint32_t nib = (__ldcg(p.tuple_done + t) >> (4 * p.group)) & 15u;
+      prev = nib == 15u ? -1 : (int)nib - 1;
+    }
+    // per-variant kept prefix at this layer (−1: the variant's cut excludes l) — computed once per
+    // unit; the snapshot logic below only compares against these
+    int nkv[kMaxVar];
+#pragma unroll
+    for (int v = 0; v < kMaxVar; ++v)
+      nkv[v] = (v < p.n_var && p.cut[v] > l) ? n_kept(L, p.keep[v]) : -1;
+    int s0 = 0, s1 = 0;
+#pragma unroll
+    for (int v = 0; v < kMaxVar; ++v) {
+      if (v <= v_hi) s1 = max(s1, nkv[v]);
+      if (v <= prev) s0 = max(s0, nkv[v]);
+    }
+    // snapshot points in (s0, s1]: any variant, any rank
+    auto next_point = [&](int after) {
+      int nx = 0x7fffffff;
+#pragma unroll
+      for (int v = 0; v < kMaxVar; ++v)
+        if (nkv[v] > after) nx = min(nx, nkv[v]);
+      return nx;
+    };
+    const int first_snap = next_point(s0);
+    const int n_need = s1;
 
     const int64_t pbase = p.page_indptr[t];
-    const int n_pages = (n_need + 15) >> 4;
-    int pid_chunk = 0;
-    int pid_reg = lane < n_pages ? __ldg(p.page_ids + pbase + lane) : 0;
+    const int pg0 = s0 >> 4;
+    const int pg1 = (s1 + 15) >> 4;
+    const int npu = s1 > s0 ? pg1 - pg0 : 0;  // pages streamed per kv-head
+    int pid_chunk = pg0 >> 5;
+    int pid_reg = 0;
+    {
+      const int idx = (pid_chunk << 5) + lane;
+      if (idx < pg1) pid_reg = __ldg(p.page_ids + pbase + idx);
+    }
 
-    // TMA issue of stream page k = hh·n_pages + pg of this unit (head h0 + hh) into the next
-    // ring slot (whole warp calls; lane 0 issues)
-    auto issue = [&](int k) {
-      const int hh = k / n_pages, pg = k - hh * n_pages;
-      const int h = h0 + hh;
+    // TMA issue of the unit's next stream page (cursor: head iss_h, page iss_pg) into the next ring
+    // slot (whole warp calls; lane 0 issues)
+    int iss_h = 0, iss_pg = pg0, n_iss = 0;
+    auto issue = [&]() {
+      const int h = h0 + iss_h, pg = iss_pg;
       const int chunk = pg >> 5;
       if (chunk != pid_chunk) {
         const int idx = (chunk << 5) + lane;
-        pid_reg = idx < n_pages ? __ldg(p.page_ids + pbase + idx) : 0;
+        pid_reg = idx < pg1 ? __ldg(p.page_ids + pbase + idx) : 0;
         pid_chunk = chunk;
       }
       const int pid = __shfl_sync(0xffffffffu, pid_reg, pg & 31);
@@ -304,64 +359,92 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
           tma_load_box(dst + b * Ring<D>::kBoxBytes, &p.tmap, 64 * b, h, 2 * l, pid, bar, policy);
       }
       ++issued;
+      ++n_iss;
+      if (++iss_pg == pg1) { iss_pg = pg0; ++iss_h; }
     };
     // prologue: fill the ring (all earlier stages have been consumed)
-    const int n_stream = HG * n_pages;
+    const int n_stream = HG * npu;
     const int n_pro = min(S, n_stream);
-    for (int k = 0; k < n_pro; ++k) issue(k);
+    for (int k = 0; k < n_pro; ++k) issue();
 
-   for (int hh = 0; hh < HG; ++hh) {
+    // operator-query / readout fragments of (l, h): loaded for the unit's first head here and for
+    // every later head right after the last page's MMAs of the previous one (latency hidden
+    // behind that page's softmax work)
+    uint32_t qa[KS][4];
+    uint32_t wa1[WREG > 0 ? WREG : 1][KS][4];
+    auto load_frags = [&](int h) {
+      const int lh = l * Hkv + h;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const uint4 f = __ldg(p.qfrag + ((size_t)lh * KS + ks) * 32 + lane);
+        qa[ks][0] = f.x; qa[ks][1] = f.y; qa[ks][2] = f.z; qa[ks][3] = f.w;
+      }
+#pragma unroll
+      for (int tt = 0; tt < WREG; ++tt)
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint4 f = __ldg(p.wfrag + (((size_t)lh * NT + tt) * KS + ks) * 32 + lane);
+          wa1[tt][ks][0] = f.x; wa1[tt][ks][1] = f.y; wa1[tt][ks][2] = f.z; wa1[tt][ks][3] = f.w;
+        }
+    };
+    if (npu > 0) load_frags(h0);
+
+   for (int hh = 0; hh < (npu > 0 ? HG : 0); ++hh) {
     const int h = h0 + hh;
     const int unit_lh = l * Hkv + h;  // partial-logit slot of (layer, kv-head)
     int next_snap = first_snap;
-
-    // operator-query fragments for (l, h)
-    const int lh = l * Hkv + h;
-    uint32_t qa[KS][4];
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const uint4 f = __ldg(p.qfrag + ((size_t)lh * KS + ks) * 32 + lane);
-      qa[ks][0] = f.x; qa[ks][1] = f.y; qa[ks][2] = f.z; qa[ks][3] = f.w;
-    }
-    uint32_t wa1[WREG > 0 ? WREG : 1][KS][4];
-#pragma unroll
-    for (int tt = 0; tt < WREG; ++tt)
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const uint4 f = __ldg(p.wfrag + (((size_t)lh * NT + tt) * KS + ks) * 32 + lane);
-        wa1[tt][ks][0] = f.x; wa1[tt][ks][1] = f.y; wa1[tt][ks][2] = f.z; wa1[tt][ks][3] = f.w;
-      }
-    const uint4* wbase = p.wfrag + (size_t)lh * NT * KS * 32 + lane;
+    const uint4* wbase = p.wfrag + (size_t)unit_lh * NT * KS * 32 + lane;
+    // saved state of (t, l, h) for this lane group (walk mode)
+    float* rst = walk ? p.rstate + ((((size_t)t * p.n_layers + l) * Hkv + h) * 8 + g) * p.rstate_w
+                      : nullptr;
 
     // lane-local online-softmax state per half-slot (log2 domain)
-    float mx[NH], sm[NH], ac[NH][CPR];
+    float mx[NH], sm[NH], ac[TBL ? 1 : NH][CPR], at[NSL];
 #pragma unroll
     for (int hs = 0; hs < NH; ++hs) {
       mx[hs] = -CUDART_INF_F;
       sm[hs] = 0.f;
 #pragma unroll
-      for (int c = 0; c < CPR; ++c) ac[hs][c] = 0.f;
+      for (int c = 0; c < CPR; ++c)
+        if (!TBL) ac[TBL ? 0 : hs][c] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < NSL; ++k) at[k] = 0.f;
+    if constexpr (TBL) {
+      if (walk && s0 > 0 && q == 0) {  // resume: the quad's merged state enters through lane q = 0
+        mx[0] = __ldcg(rst + 0);
+        mx[1] = __ldcg(rst + 1);
+        sm[0] = __ldcg(rst + 2);
+        sm[1] = __ldcg(rst + 3);
+#pragma unroll
+        for (int k = 0; k < NSL; ++k) at[k] = __ldcg(rst + 4 + k);
+      }
     }
 
-    int snap_lo = 0;  // first token not yet folded into the running state
+    int snap_lo = s0;  // first token not yet folded into the running state
 
-    for (int pg = 0; pg < n_pages; ++pg) {
+    for (int pg = pg0; pg < pg1; ++pg) {
       const int slot = consumed % S;
       mbar_wait(&s_full[warp][slot], (consumed / S) & 1u);
       const uint32_t stage = ring_s + slot * STAGE;
       // ---- tensor cores: S = Q·Kᵀ and U = W·Vᵀ for this page's 16 tokens
+      const bool tail_page = pg * 16 + 16 > n_need;  // warp-uniform
       float Sacc[2][4];
       float U[NT][2][4];
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
-        const bool valid = (pg * 16 + nt * 8 + g) < n_need;  // B-operand row = token nt*8+g
         uint4 kf[KP], vf[KP];
 #pragma unroll
         for (int j = 0; j < KP; ++j) {
           const uint32_t a = stage + frag_off[j] + nt * 8 * 128;
           kf[j] = lds128(a);
           vf[j] = lds128(a + 16 * 128);  // V rows follow the 16 K rows of the box
-          if (!valid) { kf[j] = make_uint4(0, 0, 0, 0); vf[j] = make_uint4(0, 0, 0, 0); }
+        }
+        if (tail_page) {  // tokens past the extent (unused slots may hold anything, even NaN)
+          const bool valid = (pg * 16 + nt * 8 + g) < n_need;  // B-operand row = token nt*8+g
+#pragma unroll
+          for (int j = 0; j < KP; ++j)
+            if (!valid) { kf[j] = make_uint4(0, 0, 0, 0); vf[j] = make_uint4(0, 0, 0, 0); }
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) Sacc[nt][i] = 0.f;
@@ -401,15 +484,51 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       // the stage's bytes are in registers: hand the slot back to TMA for page pg + S
       __syncwarp();
       ++consumed;
-      if (hh * n_pages + pg + S < n_stream) {
+      if (n_iss < n_stream) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(hh * n_pages + pg + S);
+        issue();
       }
+      // the fragments are dead after the last page's MMAs: fetch the next head's now
+      if (pg + 1 == pg1 && hh + 1 < HG) load_frags(h + 1);
       // ---- per-lane token indices and values: k = nt*2 + e ↔ token pg*16 + nt*8 + 2q + e
       const int page_hi = min(pg * 16 + 16, n_need);
       for (;;) {
         const int seg_hi = min(next_snap, page_hi);
         // fold tokens [snap_lo, seg_hi) of this page into the lane-local state
+        if constexpr (TBL) {
+          float corr[2], ps[2][4];
+#pragma unroll
+          for (int hs = 0; hs < 2; ++hs) {
+            float x[4];
+            float xm = -CUDART_INF_F;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int nt = k >> 1, e = k & 1;
+              const int tok = pg * 16 + nt * 8 + 2 * q + e;
+              const bool in = tok >= snap_lo && tok < seg_hi;
+              x[k] = in ? Sacc[nt][2 * hs + e] * p.scale_log2 : -CUDART_INF_F;
+              xm = fmaxf(xm, x[k]);
+            }
+            const float mn = fmaxf(mx[hs], xm);
+            const bool live = mn != -CUDART_INF_F;
+            corr[hs] = live ? ex2(mx[hs] - mn) : 1.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ps[hs][k] = live ? ex2(x[k] - mn) : 0.f;
+            sm[hs] = sm[hs] * corr[hs] + ((ps[hs][0] + ps[hs][1]) + (ps[hs][2] + ps[hs][3]));
+            mx[hs] = mn;
+          }
+#pragma unroll
+          for (int k = 0; k < NSL; ++k) {
+            const bool hi = (tsel >> k) & 1u;
+            float a = at[k] * (hi ? corr[1] : corr[0]);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const int nt = kk >> 1, e = kk & 1;
+              a = fmaf(hi ? ps[1][kk] : ps[0][kk], U[k >> 1][nt][2 * (k & 1) + e], a);
+            }
+            at[k] = a;
+          }
+        } else {
 #pragma unroll
         for (int hs = 0; hs < NH; ++hs) {
           float x[4];
@@ -432,21 +551,74 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 #pragma unroll
             for (int c = 0; c < (hs == 0 ? CPR0 : CPR1); ++c) {
               const int tt = NOLO ? (hs == 0 ? 0 : T0) + c / 2 : (hs == 0 ? c : CPR0 + c);
-              float a = ac[hs][c] * corr;
+              float a = ac[TBL ? 0 : hs][c] * corr;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const int nt = k >> 1, e = k & 1;
                 const float u = NOLO ? U[tt][nt][2 * (c & 1) + e] : U[tt][nt][e] + U[tt][nt][2 + e];
                 a = fmaf(ps[k], u, a);
               }
-              ac[hs][c] = a;
+              ac[TBL ? 0 : hs][c] = a;
             }
             mx[hs] = mn;
           }
         }
+        }
         snap_lo = seg_hi;
         if (seg_hi == next_snap) {
           // ---- snapshot: merge the quad's lane states, reduce rows per op, emit partials
+          float opv[kMaxOps][CPR];  // legacy packing: per-(op, class) partial (all lanes)
+          if constexpr (TBL) {
+            float Mq[2], f[2], den[2];
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs) {
+              float M = mx[hs];
+              M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
+              M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
+              f[hs] = mx[hs] == -CUDART_INF_F ? 0.f : ex2(mx[hs] - M);
+              float d = sm[hs] * f[hs];
+              d += __shfl_xor_sync(0xffffffffu, d, 1);
+              d += __shfl_xor_sync(0xffffffffu, d, 2);
+              den[hs] = d;
+              Mq[hs] = M;
+            }
+            float accm[NSL], val[NSL];
+#pragma unroll
+            for (int k = 0; k < NSL; ++k) {
+              const bool hi = (tsel >> k) & 1u;
+              float a = at[k] * (hi ? f[1] : f[0]);
+              a += __shfl_xor_sync(0xffffffffu, a, 1);
+              a += __shfl_xor_sync(0xffffffffu, a, 2);
+              accm[k] = a;
+              val[k] = tgt[k] >= 0 ? __fdiv_rn(a, hi ? den[1] : den[0]) : 0.f;
+            }
+            if (walk && p.save_state && next_snap == s1 && q == 0) {
+              // end of this round's extent: save the merged state for a later round to resume
+              rst[0] = Mq[0]; rst[1] = Mq[1]; rst[2] = den[0]; rst[3] = den[1];
+#pragma unroll
+              for (int k = 0; k < NSL; ++k) rst[4 + k] = accm[k];
+            }
+            // cross-lane-group sum per (op, class) target through shared memory: lane j adds
+            // target j's slots in a fixed (ascending) order, then writes its partial
+            float* sv = s_z[warp];
+            if (q == 0) {
+#pragma unroll
+              for (int k = 0; k < NSL; ++k) sv[g * NSL + k] = val[k];
+            }
+            __syncwarp();
+            float x = 0.f;
+            for (uint64_t m = red0; m; m &= m - 1) x += sv[__ffsll((long long)m) - 1];
+            for (uint64_t m = red1; m; m &= m - 1) x += sv[64 + __ffsll((long long)m) - 1];
+            __syncwarp();
+            if (red0 | red1) {
+              const int o = lane >> 3, c = lane & 7;
+#pragma unroll
+              for (int v = 0; v < kMaxVar; ++v)
+                if (nkv[v] == next_snap)
+                  p.part[((((size_t)t * p.n_lh_all + unit_lh) * p.n_ops_total + p.op_ids[o]) *
+                              p.n_var_total + p.var_ids[v]) * CPR + c] = x;
+            }
+          } else {
           float val[NH][CPR];
 #pragma unroll
           for (int hs = 0; hs < NH; ++hs) {
@@ -460,13 +632,12 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 #pragma unroll
             for (int c = 0; c < CPR; ++c) {
               if (c >= (hs == 0 ? CPR0 : CPR1)) { val[hs][c] = 0.f; continue; }
-              float a = ac[hs][c] * f;
+              float a = ac[TBL ? 0 : hs][c] * f;
               a += __shfl_xor_sync(0xffffffffu, a, 1);
               a += __shfl_xor_sync(0xffffffffu, a, 2);
               val[hs][c] = __fdiv_rn(a, den);
             }
           }
-          float opv[kMaxOps][CPR];
 #pragma unroll
           for (int o = 0; o < kMaxOps; ++o) {
 #pragma unroll
@@ -482,9 +653,11 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
               opv[o][c] = x;
             }
           }
-          if (lane == 0) {
-            for (int v = 0; v < p.n_var; ++v) {
-              if (!(p.cut[v] > l) || n_kept(L, p.keep[v]) != next_snap) continue;
+          }
+          if (!TBL && lane == 0) {  // grid: partials per work slot, local (op, variant) indices
+#pragma unroll
+            for (int v = 0; v < kMaxVar; ++v) {
+              if (nkv[v] != next_snap) continue;
 #pragma unroll
               for (int o = 0; o < kMaxOps; ++o) {
                 if (o >= p.n_ops) break;
@@ -494,14 +667,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
               }
             }
           }
-          // advance to the next larger snapshot point
-          int nxt = 0x7fffffff;
-          for (int v = 0; v < p.n_var; ++v)
-            if (p.cut[v] > l) {
-              const int nk = n_kept(L, p.keep[v]);
-              if (nk > next_snap) nxt = min(nxt, nk);
-            }
-          next_snap = nxt;
+          next_snap = next_point(next_snap);  // the next larger snapshot point
         }
         if (snap_lo >= page_hi) break;
       }
@@ -525,45 +691,35 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     __threadfence();
 
     // z = b + Σ_u partial_u over the units whose layer is inside the variant's cut, for every
-    // (op, variant, class) entry: lane u loads unit u's partials (all entries issued at once, so
-    // the L2 latency is paid once, not once per unit), then a fixed xor-tree per entry — a fixed
-    // summation order, so margins stay bitwise reproducible.
+    // (op, variant, class) entry: one lane per entry sums its units in a FIXED (ascending) order in
+    // fp64, so margins stay bitwise reproducible.  Grid: this launch's partials per work slot,
+    // local (op, variant); walk: per tuple over all layers, caller's (op, variant), only the
+    // variants complete after this round (avail_mask).
     float* zs = s_z[warp];
     const int nz = p.n_ops * p.n_var * CPR;
-    const int n_pu = p.n_l * Hkv;  // partial slots per tuple (layer-major)
-    const float* tpart = p.part + (size_t)wslot * n_pu * nz;
-    for (int e0 = 0; e0 < nz; e0 += 8) {
-      double acc[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] = 0.0;
-      for (int u0 = 0; u0 < n_pu; u0 += 32) {
-        const int uu = u0 + lane;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int idx = e0 + k;
-          if (idx < nz && uu < n_pu) {
-            const int v = (idx / CPR) % p.n_var;
-            if (uu < min(p.cut[v], p.n_l) * Hkv)  // units are l-major: l < cut ⇔ u < cut·Hkv
-              acc[k] += (double)__ldcg(tpart + (size_t)uu * nz + idx);
-          }
-        }
+    const int n_pu = walk ? p.n_lh_all : p.n_l * Hkv;  // partial slots per tuple (layer-major)
+    const int nzg = walk ? p.n_ops_total * p.n_var_total * CPR : nz;
+    const float* tpart = p.part + (size_t)(walk ? t : wslot) * n_pu * nzg;
+    for (int idx = lane; idx < nz; idx += 32) {
+      const int c = idx % CPR, ov = idx / CPR;
+      const int o = ov / p.n_var, v = ov - o * p.n_var;
+      if (c >= p.op_classes[o] || (walk && !((p.avail_mask >> v) & 1))) continue;
+      const float* src = tpart + (walk ? (p.op_ids[o] * p.n_var_total + p.var_ids[v]) * CPR + c : idx);
+      const int nu = min(p.cut[v], p.n_layers) * Hkv;  // l-major: l < cut ⇔ u < cut·Hkv
+      double acc = 0.0;
+      int uu = 0;
+      for (; uu + 4 <= nu; uu += 4) {
+        const float a0 = __ldcg(src + (size_t)(uu + 0) * nzg), a1 = __ldcg(src + (size_t)(uu + 1) * nzg);
+        const float a2 = __ldcg(src + (size_t)(uu + 2) * nzg), a3 = __ldcg(src + (size_t)(uu + 3) * nzg);
+        acc += (double)a0; acc += (double)a1; acc += (double)a2; acc += (double)a3;
       }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-        const int idx = e0 + k;
-        if (lane == 0 && idx < nz) {
-          const int c = idx % CPR, o = idx / (CPR * p.n_var);
-          zs[idx] = c < p.op_classes[o] ? (float)((double)__ldg(p.bias[o] + c) + acc[k])
-                                        : -CUDART_INF_F;
-        }
-      }
+      for (; uu < nu; ++uu) acc += (double)__ldcg(src + (size_t)uu * nzg);
+      zs[idx] = (float)((double)__ldg(p.bias[o] + c) + acc);
     }
     __syncwarp();
-    const bool walk = p.mode == MODE_WALK;
     for (int idx = lane; idx < p.n_ops * p.n_var; idx += 32) {
       const int o = idx / p.n_var, v = idx % p.n_var;
+      if (walk && !((p.avail_mask >> v) & 1)) continue;
       const float* zz = zs + idx * CPR;
       float m;
       int cls = 0;
@@ -690,7 +846,8 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
     for (int i = threadIdx.x; i < p.n_plans * (int)(sizeof(ko_plan) / 4); i += blockDim.x)
       reinterpret_cast<uint32_t*>(p.gplans)[i] = reinterpret_cast<const uint32_t*>(p.plans)[i];
   const int KS = p.head_dim / 16;
-  const int NT = p.nolo ? (p.CPR0 + 1) / 2 + (p.CPR1 + 1) / 2 : p.CPR0 + p.CPR1;
+  const int NT = p.tbl_nt > 0 ? p.tbl_nt
+               : p.nolo ? (p.CPR0 + 1) / 2 + (p.CPR1 + 1) / 2 : p.CPR0 + p.CPR1;
   const int Hq = p.n_kv_heads * p.gqa;
   const int n_lh = p.n_l * p.n_kv_heads;
   const int64_t nq_items = (int64_t)n_lh * KS * 32;
@@ -718,6 +875,27 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
             const int o = p.slot_op[rho], rem = p.slot_rem[rho];
             const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
             b = p.q[o][(((size_t)l * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k];
+          }
+          vals[hr][k] = b;
+        }
+      }
+    } else if (p.tbl_nt > 0) {
+      // table packing: A-row half hr of tile tt at lane group g = slot 2·tt + hr of the table
+      for (int hr = 0; hr < 2; ++hr) {
+        const int ent = p.tbl_w[g][2 * tt + hr];
+        for (int k = 0; k < 4; ++k) {
+          uint16_t b = 0;
+          if (ent >= 0) {
+            const int o = ent & 7, rem = (ent >> 3) & 31, c = (ent >> 8) & 15, lo = (ent >> 12) & 1;
+            const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
+            const size_t wi = ((((size_t)c * p.n_layers + l) * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k;
+            if (p.w_bf16[o]) {
+              b = lo ? 0 : p.w_bf16[o][wi];
+            } else {
+              const float w = p.w[o][wi];
+              const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+              b = __bfloat16_as_ushort(lo ? __float2bfloat16_rn(w - __bfloat162float(hi)) : hi);
+            }
           }
           vals[hr][k] = b;
         }
@@ -947,15 +1125,14 @@ int num_sms() {
   return n;
 }
 
-template <int D, int CPR0, int CPR1, bool NOLO>
+template <int D, int CPR0, int CPR1, bool NOLO, int TNT>
 cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t s) {
   static int occ = 0;
   constexpr int smem = Ring<D>::kSmemBytes;
+  auto* kern = ko_score_kernel<D, CPR0, CPR1, NOLO, TNT>;
   if (!occ) {
-    cudaFuncSetAttribute(ko_score_kernel<D, CPR0, CPR1, NOLO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ko_score_kernel<D, CPR0, CPR1, NOLO>, kThreads,
-                                                  smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
     if (occ < 1) occ = 1;
   }
   const int64_t warps_needed = max_units > 0 ? max_units : 1;
@@ -963,7 +1140,7 @@ cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t
   const int64_t need = (warps_needed + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  ko_score_kernel<D, CPR0, CPR1, NOLO><<<(unsigned)grid, kThreads, smem, s>>>(p);
+  kern<<<(unsigned)grid, kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1073,23 +1250,31 @@ cudaError_t launch_prep(const PrepParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, bool nolo,
-                         int64_t max_units, cudaStream_t s) {
+                         int tnt, int64_t max_units, cudaStream_t s) {
 #define KO_DISPATCH(DD, C0, C1)                                                       \
-  if (head_dim == DD && CPR0 == C0 && CPR1 == C1 && !nolo)                           \
-    return launch_score_t<DD, C0, C1, false>(p, max_units, s);
+  if (head_dim == DD && CPR0 == C0 && CPR1 == C1 && !nolo && tnt == 0)               \
+    return launch_score_t<DD, C0, C1, false, 0>(p, max_units, s);
 #define KO_DISPATCH_NOLO(DD, C0, C1)                                                  \
-  if (head_dim == DD && CPR0 == C0 && CPR1 == C1 && nolo)                            \
-    return launch_score_t<DD, C0, C1, true>(p, max_units, s);
+  if (head_dim == DD && CPR0 == C0 && CPR1 == C1 && nolo && tnt == 0)                \
+    return launch_score_t<DD, C0, C1, true, 0>(p, max_units, s);
+#define KO_DISPATCH_TBL(DD, C0, T)                                                    \
+  if (head_dim == DD && CPR0 == C0 && tnt == T)                                      \
+    return launch_score_t<DD, C0, 0, false, T>(p, max_units, s);
 #define KO_DISPATCH_D(DD)                                                                  \
   KO_DISPATCH(DD, 1, 0) KO_DISPATCH(DD, 1, 1) KO_DISPATCH(DD, 2, 0) KO_DISPATCH(DD, 2, 1)   \
   KO_DISPATCH(DD, 2, 2) KO_DISPATCH(DD, 4, 0) KO_DISPATCH(DD, 4, 1) KO_DISPATCH(DD, 4, 2)   \
   KO_DISPATCH(DD, 4, 4) KO_DISPATCH(DD, 8, 0) KO_DISPATCH(DD, 8, 1) KO_DISPATCH(DD, 8, 2)   \
   KO_DISPATCH(DD, 8, 4) KO_DISPATCH(DD, 8, 8)                                              \
   KO_DISPATCH_NOLO(DD, 2, 0) KO_DISPATCH_NOLO(DD, 4, 0) KO_DISPATCH_NOLO(DD, 8, 0)          \
-  KO_DISPATCH_NOLO(DD, 2, 1) KO_DISPATCH_NOLO(DD, 4, 1) KO_DISPATCH_NOLO(DD, 8, 1)
+  KO_DISPATCH_NOLO(DD, 2, 1) KO_DISPATCH_NOLO(DD, 4, 1) KO_DISPATCH_NOLO(DD, 8, 1)          \
+  KO_DISPATCH_TBL(DD, 1, 1) KO_DISPATCH_TBL(DD, 1, 2) KO_DISPATCH_TBL(DD, 1, 4)             \
+  KO_DISPATCH_TBL(DD, 2, 1) KO_DISPATCH_TBL(DD, 2, 2) KO_DISPATCH_TBL(DD, 2, 4)             \
+  KO_DISPATCH_TBL(DD, 4, 2) KO_DISPATCH_TBL(DD, 4, 4)                                      \
+  KO_DISPATCH_TBL(DD, 8, 4) KO_DISPATCH_TBL(DD, 8, 8)
   KO_DISPATCH_D(64)
   KO_DISPATCH_D(128)
 #undef KO_DISPATCH_D
+#undef KO_DISPATCH_TBL
 #undef KO_DISPATCH_NOLO
 #undef KO_DISPATCH
   return cudaErrorInvalidValue;
