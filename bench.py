@@ -285,6 +285,7 @@ def main():
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
+    launches_per_step = ko.last_launch_count()   # the library's kernels in one step's call
     ms_total = e0.elapsed_time(e1)
     kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_pairs]))
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
@@ -344,7 +345,7 @@ def main():
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src},
             "cpu_baseline": cb,
             "e2e": e2e,
-            "gpu_launches": (3 * len(plans[0]) + 2 if routed else 2) * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
             "counts_plan0": cnt[0, :5].tolist(),
             "plan_selection": selection,

@@ -245,6 +245,11 @@ double ko_beta_lower_bound(int64_t a, int64_t b, double alpha);
  * the hot kernel alone with cudaEventElapsedTime.  Pass NULL, NULL to disable. */
 void ko_set_trace_events(void* ev_begin, void* ev_end);
 
+/* Number of kernels the last compute call on this thread (ko_score_batch, ko_route,
+ * ko_reduce_stats, ko_embed_scores, ko_build_importance_order, ko_soft_stats) launched — how
+ * bench.py counts the library's own launches inside its timed region. */
+int32_t ko_last_launch_count(void);
+
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char* ko_last_error(void);
 

@@ -88,13 +88,14 @@ def _load():
     L.ko_set_trace_events.restype = None
     L.ko_last_error.restype = ctypes.c_char_p
     L.ko_version.restype = ctypes.c_char_p
+    L.ko_last_launch_count.restype = ctypes.c_int32
     return L
 
 
 _lib = _load()
 EXPORTS = ("ko_score_batch", "ko_route", "ko_reduce_stats", "ko_workspace_size",
            "ko_embed_scores", "ko_build_importance_order", "ko_soft_stats", "ko_soft_workspace_size", "ko_beta_lower_bound",
-           "ko_set_trace_events", "ko_last_error", "ko_version")
+           "ko_set_trace_events", "ko_last_error", "ko_version", "ko_last_launch_count")
 
 
 def lib():
@@ -107,6 +108,11 @@ def last_error() -> str:
 
 def version() -> str:
     return _lib.ko_version().decode()
+
+
+def last_launch_count() -> int:
+    """Kernels launched by the last compute call on this thread (ko_last_launch_count)."""
+    return int(_lib.ko_last_launch_count())
 
 
 def _check(rc: int):

@@ -21,6 +21,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local cudaEvent_t g_trace_begin = nullptr, g_trace_end = nullptr;
+thread_local int32_t g_launches = 0;  // kernels launched by the last compute call (ko_last_launch_count)
 
 ko_status fail(ko_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 ko_status fail(ko_status st, const char* fmt, ...) {
@@ -32,6 +33,13 @@ ko_status fail(ko_status st, const char* fmt, ...) {
   g_err = buf;
   return st;
 }
+
+// a kernel launch of this library: counted for ko_last_launch_count, then checked
+#define KO_LAUNCH(expr)                                                                \
+  do {                                                                                 \
+    ++g_launches;                                                                      \
+    KO_CUDA(expr);                                                                     \
+  } while (0)
 
 #define KO_CUDA(expr)                                                                  \
   do {                                                                                 \
@@ -231,10 +239,13 @@ ko_status make_tmap(CUtensorMap* map, const ko_kv_cache* kv) {
 // (caller indices op_sel[0..n_sel)) and variants.  Row slots: the selected ops are laid out in
 // descending class count, n_q·gqa rows each, slot = half·8 + g; CPR0 / CPR1 (returned) are the
 // power-of-two class counts of the two halves of the 16-row tile (CPR1 = 0: one half used).
-// Table packing (walk mode): every S row (op, gqa member, query row) of the selected ops goes to
-// one of 8 lane groups holding ≤ 2 rows (S rows g and g + 8); a row of a C-class op needs C W·V
-// entries (2C for fp32 W: bf16 hi and lo), and a lane group's entries fill the 2·NT slots of NT
-// tiles.  Smallest supported NT by first-fit decreasing; 0 if none ≤ kMaxTNT fits.
+// Table packing (walk mode).  Lane group g owns S rows g (half 0) and g + 8 (half 1); W·V tile tt
+// gives it slot (tt, hr) = A row g + 8·hr, which always accumulates with S-row half hr.  So each
+// half of a lane group offers NT slots.  An S row (op, gqa member, query row) of a C-class op needs
+// C entries (2C for fp32 W: bf16 hi and lo).  A row with ≤ NT entries takes one half; a row with
+// NT < e ≤ 2·NT entries is duplicated into both halves of a lane group (the same query in S rows g
+// and g + 8) and its entries are split between them.  Smallest NT ∈ {1, 2, 4, 8} that fits, big
+// rows first; returns 0 if none fits.
 int pack_table(const ko_operator* ops, const int* order, int n_sel, int rows_per_op,
                ko::ScoreParams& sp, ko::PrepParams& pp) {
   struct Row { int i, rem, e; };
@@ -247,33 +258,43 @@ int pack_table(const ko_operator* ops, const int* order, int n_sel, int rows_per
     }
   std::stable_sort(rows, rows + nr, [](const Row& a, const Row& b) { return a.e > b.e; });
   for (int NT : {1, 2, 4, 8}) {
-    int bin_n[8] = {0}, bin_e[8] = {0}, bin_row[8][2];
+    int at[8][2];  // row index (into rows[]) at (lane group, half), −1 free
+    for (int b = 0; b < 8; ++b) at[b][0] = at[b][1] = -1;
     bool ok = true;
     for (int k = 0; k < nr && ok; ++k) {
-      int b = 0;
-      while (b < 8 && !(bin_n[b] < 2 && bin_e[b] + rows[k].e <= 2 * NT)) ++b;
-      if (b == 8) { ok = false; break; }
-      bin_row[b][bin_n[b]++] = k;
-      bin_e[b] += rows[k].e;
+      const int e = rows[k].e;
+      if (e > 2 * NT) { ok = false; break; }
+      bool placed = false;
+      if (e > NT) {  // both halves of a free lane group
+        for (int b = 0; b < 8 && !placed; ++b)
+          if (at[b][0] < 0 && at[b][1] < 0) { at[b][0] = at[b][1] = k; placed = true; }
+      } else {
+        for (int b = 0; b < 8 && !placed; ++b)
+          for (int hs = 0; hs < 2 && !placed; ++hs)
+            if (at[b][hs] < 0) { at[b][hs] = k; placed = true; }
+      }
+      ok = placed;
     }
     if (!ok) continue;
     for (int r = 0; r < 16; ++r) { sp.slot_op[r] = -1; pp.slot_op[r] = -1; pp.slot_rem[r] = 0; }
     for (int b = 0; b < 8; ++b) {
-      sp.tbl_sel[b] = 0;
       for (int k = 0; k < 16; ++k) { sp.tbl_tgt[b][k] = -1; pp.tbl_w[b][k] = -1; }
-      int k = 0;
-      for (int hs = 0; hs < bin_n[b]; ++hs) {
-        const Row& R = rows[bin_row[b][hs]];
+      for (int hs = 0; hs < 2; ++hs) {
+        if (at[b][hs] < 0) continue;
+        const Row& R = rows[at[b][hs]];
         sp.slot_op[hs * 8 + b] = R.i;
         pp.slot_op[hs * 8 + b] = R.i;
         pp.slot_rem[hs * 8 + b] = R.rem;
         const ko_operator& op = ops[order[R.i]];
-        for (int c = 0; c < op.n_classes; ++c)
-          for (int lo = 0; lo < (op.w_is_bf16 ? 1 : 2); ++lo, ++k) {
-            pp.tbl_w[b][k] = R.i | (R.rem << 3) | (c << 8) | (lo << 12);
-            sp.tbl_tgt[b][k] = (int8_t)(R.i * 8 + c);
-            if (hs) sp.tbl_sel[b] |= 1u << k;
-          }
+        const int nlo = op.w_is_bf16 ? 1 : 2;
+        const bool dup = at[b][0] == at[b][1];
+        const int e0 = dup ? (R.e + 1) / 2 : R.e;  // entries on half 0 (all of them if not split)
+        const int lo_e = dup && hs == 1 ? e0 : 0, hi_e = dup && hs == 0 ? e0 : R.e;
+        for (int ent = lo_e, tt = 0; ent < hi_e; ++ent, ++tt) {
+          const int c = ent / nlo, lo = ent % nlo;
+          pp.tbl_w[b][2 * tt + hs] = R.i | (R.rem << 3) | (c << 8) | (lo << 12);
+          sp.tbl_tgt[b][2 * tt + hs] = (int8_t)(R.i * 8 + c);
+        }
       }
     }
     return NT;
@@ -411,6 +432,8 @@ void ko_set_trace_events(void* ev_begin, void* ev_end) {
   g_trace_end = (cudaEvent_t)ev_end;
 }
 
+int32_t ko_last_launch_count(void) { return g_launches; }
+
 const char* ko_version(void) { return "ko 0.1 (sm_100a, mma.sync bf16 W-folded paged attention)"; }
 
 size_t ko_workspace_size(const ko_kv_cache* kv, const ko_operator* ops, int32_t n_ops,
@@ -426,6 +449,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
                          int64_t n_idx, float* margins, int32_t* classes, const ko_plan* plans,
                          int32_t n_plans, const uint8_t* gold, int64_t* counts, void* workspace,
                          size_t workspace_bytes, void* stream) {
+  g_launches = 0;
   ko_status st;
   if ((st = validate_kv(kv)) != KO_OK) return st;
   if ((st = validate_ops(kv, ops, n_ops)) != KO_OK) return st;
@@ -489,11 +513,11 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     pp.gplans = ws.gplans;
     pp.n_plans = n_plans;
     for (int g = 0; g < n_plans; ++g) pp.plans[g] = plans[g];
-    KO_CUDA(ko::launch_prep(pp, s));
+    KO_LAUNCH(ko::launch_prep(pp, s));
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0, 0,
+    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0, 0,
                              n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end) KO_CUDA(cudaEventRecord(g_trace_end, s));
     return KO_OK;
@@ -611,7 +635,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   // A position whose (group, round) is covered by position 0 never receives a tuple (position 0
   // processes every tuple), so it is not launched.
   KO_CUDA(cudaMemsetAsync(ws.round_len, 0, sizeof(unsigned long long) * KO_MAX_STAGES, s));
-  int last_launch = 0;
+  int last_launch = 0, prepped_group = -1;
   for (int pos = 0; pos < P.n_stages; ++pos)
     if (pos == 0 || !(pos_group[pos] == pos_group[0] && std::max(pos_round[pos], 0) <= std::max(pos_round[0], 0)))
       last_launch = pos;
@@ -671,15 +695,18 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     sp.wm = ws.wm;
     sp.wc = ws.wc;
     sp.counts = (unsigned long long*)counts;
-    KO_CUDA(ko::launch_prep(pp, s));
+    if (g != prepped_group) {  // the fragments depend only on the group (all plan layers)
+      KO_LAUNCH(ko::launch_prep(pp, s));
+      prepped_group = g;
+    }
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin && pos == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_CUDA(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, false, TNT,
+    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, false, TNT,
                              n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end && pos == last_launch) KO_CUDA(cudaEventRecord(g_trace_end, s));
   }
-  KO_CUDA(ko::launch_final_counts(rp, s));
+  KO_LAUNCH(ko::launch_final_counts(rp, s));
   return KO_OK;
 }
 
@@ -687,6 +714,7 @@ ko_status ko_route(const ko_plan* plan, const float* margins, const int32_t* cla
                    const int32_t* n_classes, int32_t n_ops, int32_t n_variants, int64_t n_tuples,
                    int32_t stage, uint32_t* tuple_state, int32_t* worklist_out,
                    int64_t* worklist_len, const uint8_t* gold, int64_t* counts, void* stream) {
+  g_launches = 0;
   if (!plan || !margins || !n_classes || !tuple_state || !counts)
     return fail(KO_EINVAL, "ko_route: NULL plan/margins/n_classes/tuple_state/counts");
   if (n_ops < 1 || n_ops > KO_MAX_OPS) return fail(KO_EINVAL, "n_ops %d", n_ops);
@@ -723,14 +751,14 @@ ko_status ko_route(const ko_plan* plan, const float* margins, const int32_t* cla
   }
   if (worklist_len) KO_CUDA(cudaMemsetAsync(worklist_len, 0, 8, s));
   if (stage == -1) {
-    KO_CUDA(ko::launch_route_plan(rp, s));
+    KO_LAUNCH(ko::launch_route_plan(rp, s));
     return KO_OK;
   }
   rp.stage = stage;
-  KO_CUDA(ko::launch_route_apply(rp, s));
+  KO_LAUNCH(ko::launch_route_apply(rp, s));
   if (worklist_out) {
     rp.stage = stage + 1;  // tuples reaching the next stage (none after the last)
-    KO_CUDA(ko::launch_route_reach(rp, s));
+    KO_LAUNCH(ko::launch_route_reach(rp, s));
   }
   return KO_OK;
 }
@@ -739,6 +767,7 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
                           const int32_t* classes, const int32_t* n_classes, int32_t n_ops,
                           int32_t n_variants, int64_t n_tuples, const uint8_t* gold,
                           int64_t* counts, void* stream) {
+  g_launches = 0;
   if (!plans || !margins || !n_classes || !counts)
     return fail(KO_EINVAL, "ko_reduce_stats: NULL plans/margins/n_classes/counts");
   if (n_plans < 1 || n_plans > KO_MAX_PLANS) return fail(KO_EINVAL, "n_plans %d", n_plans);
@@ -767,7 +796,7 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
   rp.gold = gold;
   rp.counts = (unsigned long long*)counts;
   for (int g = 0; g < n_plans; ++g) rp.plans[g] = plans[g];
-  KO_CUDA(ko::launch_reduce(rp, (cudaStream_t)stream));
+  KO_LAUNCH(ko::launch_reduce(rp, (cudaStream_t)stream));
   return KO_OK;
 }
 
@@ -775,6 +804,7 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
                           int32_t n_emb, const int32_t* op_ids, int32_t n_ops, int32_t variant,
                           int32_t n_variants, const int32_t* tuple_idx, int64_t n_idx,
                           float* margins, void* stream) {
+  g_launches = 0;
   if (!item_emb || !op_emb || !op_ids || !margins) return fail(KO_EINVAL, "ko_embed_scores: NULL argument");
   if (dim < 8 || dim % 8 != 0 || dim > 1024) return fail(KO_EINVAL, "dim %d: multiple of 8 in [8,1024]", dim);
   if (n_emb < 1 || n_emb > KO_MAX_OPS) return fail(KO_EINVAL, "n_emb %d outside [1,%d]", n_emb, KO_MAX_OPS);
@@ -800,12 +830,13 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
   ep.n_idx = n_idx;
   ep.margins = margins;
   if ((tuple_idx ? n_idx : n_tuples) == 0) return KO_OK;
-  KO_CUDA(ko::launch_embed(ep, (cudaStream_t)stream));
+  KO_LAUNCH(ko::launch_embed(ep, (cudaStream_t)stream));
   return KO_OK;
 }
 
 ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, const float* sigma2,
                                     void* dst_pool, const int32_t* dst_page_ids, void* stream) {
+  g_launches = 0;
   ko_status st;
   if ((st = validate_kv(src)) != KO_OK) return st;
   if (!mu || !sigma2 || !dst_pool || !dst_page_ids)
@@ -829,7 +860,7 @@ ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, con
   bp.dst_ids = dst_page_ids;
   bp.inv_sqrt_d = 1.0 / std::sqrt((double)src->head_dim);
   bp.inv_2d = 1.0 / (2.0 * (double)src->head_dim);
-  KO_CUDA(ko::launch_build(bp, (cudaStream_t)stream));
+  KO_LAUNCH(ko::launch_build(bp, (cudaStream_t)stream));
   return KO_OK;
 }
 
@@ -842,6 +873,7 @@ ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const do
                         double tau, const float* margins, const int32_t* n_classes, int32_t n_ops,
                         int32_t n_variants, int64_t n_tuples, const uint8_t* gold, double* out,
                         void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
   if (!plan || !pick_scores || !stage_cost || !margins || !n_classes || !out || !workspace)
     return fail(KO_EINVAL, "ko_soft_stats: NULL argument");
   if (n_ops < 1 || n_ops > KO_MAX_OPS) return fail(KO_EINVAL, "n_ops %d", n_ops);
@@ -872,7 +904,7 @@ ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const do
   sp.n_tuples = n_tuples;
   sp.gold = gold;
   sp.items = (double*)workspace;
-  KO_CUDA(ko::launch_soft(sp, out, (cudaStream_t)stream));
+  KO_LAUNCH(ko::launch_soft(sp, out, (cudaStream_t)stream));
   return KO_OK;
 }
 

@@ -97,10 +97,9 @@ struct ScoreParams {
   float* rstate;                 // [n_tuples][n_layers][Hkv][8][rstate_w] (this group's slice)
   int32_t rstate_w;              // floats per lane group: M[2], den[2], acc[2·NT]
   int32_t n_lh_all;              // n_layers · Hkv (partials of walk mode are per tuple, all layers)
-  // table-driven row/class packing (template TNT > 0): per lane group g, W·V slot k = 2·tile +
-  // (A-row half) accumulates into S row g (sel bit 0) or g + 8 (sel bit 1) for local
-  // (op, class) tgt = op·8 + class (−1: unused)
-  uint32_t tbl_sel[8];
+  // table-driven row/class packing (template TNT > 0): per lane group g, W·V slot k = 2·tile + hr
+  // (A-row half hr) accumulates with S row g + 8·hr into the local (op, class) target
+  // tgt = op·8 + class (−1: unused)
   int8_t tbl_tgt[8][16];
   ko_plan plans[kMaxPlans];
 };

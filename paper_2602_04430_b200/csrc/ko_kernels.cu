@@ -34,6 +34,9 @@ namespace ko {
 namespace {
 
 enum { D_ACCEPT = 0, D_REJECT = 1, D_UNSURE = 2, D_RESOLVED = 3 };
+// finite "no token yet" running max of the table-packed kernel: ex2(kNoMax − real) = 0 and
+// ex2(kNoMax − kNoMax) = 1, so the online-softmax update needs no −∞ special cases
+constexpr float kNoMax = -1e30f;
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -199,8 +202,8 @@ struct Ring {
 //     or 8-15 (c odd): tile(h, c) = (h ? ⌈CPR0/2⌉ : 0) + c/2, u = C[2(c&1) + e].
 // TNT > 0 (table packing, every walk-mode launch): the W·V tiles are packed per lane group g
 // from a host table — A-row half hr of tile tt at lane group g is slot k = 2·tt + hr, which
-// accumulates into S row g (sel bit 0) or g + 8 (sel bit 1) for the (op, class) tgt[k] — so a
-// K-class map row and two filter rows share TNT = ⌈entries / 2⌉ tiles.
+// accumulates with S row g + 8·hr for the (op, class) tgt[k]; a row with more entries than one
+// half's TNT slots is duplicated into both halves.
 template <int D, int CPR0, int CPR1, bool NOLO, int TNT>
 __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_constant__ ScoreParams p) {
   constexpr bool TBL = TNT > 0;
@@ -255,16 +258,17 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   int slot_op[NH];
 #pragma unroll
   for (int hs = 0; hs < NH; ++hs) slot_op[hs] = p.slot_op[hs * 8 + g];
-  // table packing: this lane group's slot → S-row half (bit k) and target (op·8 + class)
-  uint32_t tsel = 0;
+  // table packing: this lane group's slot k = 2·tile + hr (S-row half hr) → target op·8 + class
   int tgt[NSL];
 #pragma unroll
   for (int k = 0; k < NSL; ++k) tgt[k] = -1;
-  // snapshot reduction: lane j owns target j = op·8 + class; red0/red1 = its slots' positions
-  // g·NSL + k (bits 0-63 / 64-127)
+  // snapshot reduction: lane j owns target j = op·8 + class, whose slots sit at positions
+  // g·NSL + k of the warp's staging row; up to 4 positions are kept as a packed byte list (red_off,
+  // red_n), more as a bit mask over all 8·NSL positions (red0/red1, bits 0-63 / 64-127)
   uint64_t red0 = 0, red1 = 0;
+  uint32_t red_off = 0;
+  int red_n = 0;
   if constexpr (TBL) {
-    tsel = p.tbl_sel[g];
 #pragma unroll
     for (int k = 0; k < NSL; ++k) tgt[k] = p.tbl_tgt[g][k];
     for (int gg = 0; gg < 8; ++gg)
@@ -273,6 +277,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         if (p.tbl_tgt[gg][k] == lane) {
           const int i = gg * NSL + k;
           if (i < 64) red0 |= 1ull << i; else red1 |= 1ull << (i - 64);
+          if (red_n < 4) red_off |= (uint32_t)i << (8 * red_n);
+          ++red_n;
         }
   }
 
@@ -285,36 +291,114 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 
   uint32_t issued = 0, consumed = 0;  // ring positions (warp-uniform, persistent across units)
 
-  for (;;) {
+  // Work units are consumed in claim order.  Their pages enter the ring through a producer cursor
+  // that runs ahead of the consumer: once the current unit's pages are all issued, the producer
+  // decodes the NEXT unit (claimed when the current one was decoded) and keeps issuing its pages,
+  // so the ring stays full across the current unit's tail and its tuple finaliser.
+  struct Unit {
+    long long u;             // unit index (≥ n_units: none)
+    int64_t wslot, t, pbase;
+    int l, h0, L, s0, s1;    // layer, first kv-head, seq_len, streamed tokens [s0, s1)
+    int n_str;               // pages the unit streams (HG kv-heads)
+    int ih, ipg, nis;        // producer cursor: head offset, page, pages issued
+    int pid_chunk, pid_reg;  // page-id cache (chunk of 32 ids, one per lane)
+  };
+  auto claim = [&]() {
     long long u = 0;
     if (lane == 0) u = (long long)atomicAdd(p.unit_counter, 1ull);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= n_units) break;
-    const int64_t wslot = u / upt;
-    const int unit = (int)(u - wslot * upt);
-    const int l = unit / (Hkv / HG), h0 = (unit - l * (Hkv / HG)) * HG;
-    const int64_t t = p.work ? (int64_t)p.work[wslot] : wslot;
-    const int L = p.seq_len[t];
-
-    // tokens [s0, s1) this unit streams: s1 = the largest prefix among the streamed variants whose
-    // cut includes l; walk mode resumes after the extent of the tuple's previous rank (s0)
+    return u;  // meaningful in lane 0 (broadcast by decode)
+  };
+  auto decode = [&](long long u0) {
+    Unit U;
+    U.u = __shfl_sync(0xffffffffu, u0, 0);
+    U.nis = 0; U.ih = 0; U.s0 = 0; U.s1 = 0; U.pid_chunk = 0; U.pid_reg = 0;
+    U.wslot = 0; U.t = 0; U.pbase = 0; U.l = 0; U.h0 = 0; U.L = 1; U.ipg = 0; U.n_str = 0;
+    if (U.u >= n_units) return U;
+    U.wslot = U.u / upt;
+    const int unit = (int)(U.u - U.wslot * upt);
+    U.l = unit / (Hkv / HG);
+    U.h0 = (unit - U.l * (Hkv / HG)) * HG;
+    U.t = p.work ? (int64_t)p.work[U.wslot] : U.wslot;
+    U.L = p.seq_len[U.t];
+    U.pbase = p.page_indptr[U.t];
+    // tokens [s0, s1): s1 = the largest prefix among the streamed variants whose cut includes l;
+    // walk mode resumes after the extent of the tuple's previous rank for this group (s0)
     int prev = -1;
     if (walk && p.pos > 0) {
-      const uint32_t nib = (__ldcg(p.tuple_done + t) >> (4 * p.group)) & 15u;
+      const uint32_t nib = (__ldcg(p.tuple_done + U.t) >> (4 * p.group)) & 15u;
       prev = nib == 15u ? -1 : (int)nib - 1;
     }
+    for (int v = 0; v < p.n_var; ++v)
+      if (p.cut[v] > U.l) {
+        const int nk = n_kept(U.L, p.keep[v]);
+        if (v <= v_hi) U.s1 = max(U.s1, nk);
+        if (v <= prev) U.s0 = max(U.s0, nk);
+      }
+    U.ipg = U.s0 >> 4;
+    U.n_str = U.s1 > U.s0 ? HG * (((U.s1 + 15) >> 4) - U.ipg) : 0;
+    U.pid_chunk = U.ipg >> 5;
+    const int idx = (U.pid_chunk << 5) + lane;
+    if (idx < ((U.s1 + 15) >> 4)) U.pid_reg = __ldg(p.page_ids + U.pbase + idx);
+    return U;
+  };
+  auto n_pages_of = [&](const Unit& U) {  // pages streamed per kv-head
+    return U.s1 > U.s0 ? ((U.s1 + 15) >> 4) - (U.s0 >> 4) : 0;
+  };
+  // TMA issue of unit U's next stream page into the next ring slot (whole warp; lane 0 issues)
+  auto issue = [&](Unit& U) {
+    const int pg = U.ipg, pg1u = (U.s1 + 15) >> 4;
+    const int chunk = pg >> 5;
+    if (chunk != U.pid_chunk) {
+      const int idx = (chunk << 5) + lane;
+      U.pid_reg = idx < pg1u ? __ldg(p.page_ids + U.pbase + idx) : 0;
+      U.pid_chunk = chunk;
+    }
+    const int pid = __shfl_sync(0xffffffffu, U.pid_reg, pg & 31);
+    if (lane == 0) {
+      const int slot = issued % S;
+      uint64_t* bar = &s_full[warp][slot];
+      mbar_expect_tx(bar, STAGE);
+      uint8_t* dst = ring + slot * STAGE;
+#pragma unroll
+      for (int b = 0; b < D / 64; ++b)
+        tma_load_box(dst + b * Ring<D>::kBoxBytes, &p.tmap, 64 * b, U.h0 + U.ih, 2 * U.l, pid, bar,
+                     policy);
+    }
+    ++issued;
+    ++U.nis;
+    if (++U.ipg == pg1u) { U.ipg = U.s0 >> 4; ++U.ih; }
+  };
+
+  long long u_next = claim();
+  Unit cur = decode(u_next);
+  if (cur.u < n_units) u_next = claim();
+  Unit nxt;
+  bool have_nxt = false;
+  // one ring slot was freed: issue the next page of the stream (current unit, else the next one)
+  auto refill = [&]() {
+    if (cur.nis < cur.n_str) {
+      issue(cur);
+      return;
+    }
+    if (!have_nxt) {
+      nxt = decode(u_next);
+      have_nxt = true;
+      if (nxt.u < n_units) u_next = claim();
+    }
+    if (nxt.nis < nxt.n_str) issue(nxt);
+  };
+
+  while (cur.u < n_units) {
+    // top up the ring with the unit's pages (some may already be in flight from the producer)
+    while (cur.nis < cur.n_str && (int)(issued - consumed) < S) issue(cur);
+    const int64_t wslot = cur.wslot, t = cur.t;
+    const int l = cur.l, h0 = cur.h0, L = cur.L, s0 = cur.s0, s1 = cur.s1;
     // per-variant kept prefix at this layer (−1: the variant's cut excludes l) — computed once per
     // unit; the snapshot logic below only compares against these
     int nkv[kMaxVar];
 #pragma unroll
     for (int v = 0; v < kMaxVar; ++v)
       nkv[v] = (v < p.n_var && p.cut[v] > l) ? n_kept(L, p.keep[v]) : -1;
-    int s0 = 0, s1 = 0;
-#pragma unroll
-    for (int v = 0; v < kMaxVar; ++v) {
-      if (v <= v_hi) s1 = max(s1, nkv[v]);
-      if (v <= prev) s0 = max(s0, nkv[v]);
-    }
     // snapshot points in (s0, s1]: any variant, any rank
     auto next_point = [&](int after) {
       int nx = 0x7fffffff;
@@ -325,47 +409,9 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     };
     const int first_snap = next_point(s0);
     const int n_need = s1;
-
-    const int64_t pbase = p.page_indptr[t];
     const int pg0 = s0 >> 4;
     const int pg1 = (s1 + 15) >> 4;
-    const int npu = s1 > s0 ? pg1 - pg0 : 0;  // pages streamed per kv-head
-    int pid_chunk = pg0 >> 5;
-    int pid_reg = 0;
-    {
-      const int idx = (pid_chunk << 5) + lane;
-      if (idx < pg1) pid_reg = __ldg(p.page_ids + pbase + idx);
-    }
-
-    // TMA issue of the unit's next stream page (cursor: head iss_h, page iss_pg) into the next ring
-    // slot (whole warp calls; lane 0 issues)
-    int iss_h = 0, iss_pg = pg0, n_iss = 0;
-    auto issue = [&]() {
-      const int h = h0 + iss_h, pg = iss_pg;
-      const int chunk = pg >> 5;
-      if (chunk != pid_chunk) {
-        const int idx = (chunk << 5) + lane;
-        pid_reg = idx < pg1 ? __ldg(p.page_ids + pbase + idx) : 0;
-        pid_chunk = chunk;
-      }
-      const int pid = __shfl_sync(0xffffffffu, pid_reg, pg & 31);
-      if (lane == 0) {
-        const int slot = issued % S;
-        uint64_t* bar = &s_full[warp][slot];
-        mbar_expect_tx(bar, STAGE);
-        uint8_t* dst = ring + slot * STAGE;
-#pragma unroll
-        for (int b = 0; b < D / 64; ++b)
-          tma_load_box(dst + b * Ring<D>::kBoxBytes, &p.tmap, 64 * b, h, 2 * l, pid, bar, policy);
-      }
-      ++issued;
-      ++n_iss;
-      if (++iss_pg == pg1) { iss_pg = pg0; ++iss_h; }
-    };
-    // prologue: fill the ring (all earlier stages have been consumed)
-    const int n_stream = HG * npu;
-    const int n_pro = min(S, n_stream);
-    for (int k = 0; k < n_pro; ++k) issue();
+    const int npu = n_pages_of(cur);  // pages streamed per kv-head
 
     // operator-query / readout fragments of (l, h): loaded for the unit's first head here and for
     // every later head right after the last page's MMAs of the previous one (latency hidden
@@ -402,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     float mx[NH], sm[NH], ac[TBL ? 1 : NH][CPR], at[NSL];
 #pragma unroll
     for (int hs = 0; hs < NH; ++hs) {
-      mx[hs] = -CUDART_INF_F;
+      mx[hs] = TBL ? kNoMax : -CUDART_INF_F;
       sm[hs] = 0.f;
 #pragma unroll
       for (int c = 0; c < CPR; ++c)
@@ -484,10 +530,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       // the stage's bytes are in registers: hand the slot back to TMA for page pg + S
       __syncwarp();
       ++consumed;
-      if (n_iss < n_stream) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue();
-      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      refill();
       // the fragments are dead after the last page's MMAs: fetch the next head's now
       if (pg + 1 == pg1 && hh + 1 < HG) load_frags(h + 1);
       // ---- per-lane token indices and values: k = nt*2 + e ↔ token pg*16 + nt*8 + 2q + e
@@ -496,36 +540,38 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         const int seg_hi = min(next_snap, page_hi);
         // fold tokens [snap_lo, seg_hi) of this page into the lane-local state
         if constexpr (TBL) {
+          // running max starts at a finite sentinel (kNoMax): corr and p need no −∞ guards
           float corr[2], ps[2][4];
+          const bool full = pg * 16 >= snap_lo && pg * 16 + 16 <= seg_hi;  // warp-uniform
 #pragma unroll
           for (int hs = 0; hs < 2; ++hs) {
             float x[4];
-            float xm = -CUDART_INF_F;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const int nt = k >> 1, e = k & 1;
-              const int tok = pg * 16 + nt * 8 + 2 * q + e;
-              const bool in = tok >= snap_lo && tok < seg_hi;
-              x[k] = in ? Sacc[nt][2 * hs + e] * p.scale_log2 : -CUDART_INF_F;
-              xm = fmaxf(xm, x[k]);
+              x[k] = Sacc[nt][2 * hs + e] * p.scale_log2;
             }
-            const float mn = fmaxf(mx[hs], xm);
-            const bool live = mn != -CUDART_INF_F;
-            corr[hs] = live ? ex2(mx[hs] - mn) : 1.f;
+            if (!full) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) ps[hs][k] = live ? ex2(x[k] - mn) : 0.f;
+              for (int k = 0; k < 4; ++k) {
+                const int tok = pg * 16 + (k >> 1) * 8 + 2 * q + (k & 1);
+                if (!(tok >= snap_lo && tok < seg_hi)) x[k] = -CUDART_INF_F;
+              }
+            }
+            const float mn = fmaxf(fmaxf(mx[hs], fmaxf(x[0], x[1])), fmaxf(x[2], x[3]));
+            corr[hs] = ex2(mx[hs] - mn);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ps[hs][k] = ex2(x[k] - mn);
             sm[hs] = sm[hs] * corr[hs] + ((ps[hs][0] + ps[hs][1]) + (ps[hs][2] + ps[hs][3]));
             mx[hs] = mn;
           }
 #pragma unroll
           for (int k = 0; k < NSL; ++k) {
-            const bool hi = (tsel >> k) & 1u;
-            float a = at[k] * (hi ? corr[1] : corr[0]);
+            const int hr = k & 1;
+            float a = at[k] * corr[hr];
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const int nt = kk >> 1, e = kk & 1;
-              a = fmaf(hi ? ps[1][kk] : ps[0][kk], U[k >> 1][nt][2 * (k & 1) + e], a);
-            }
+            for (int kk = 0; kk < 4; ++kk)
+              a = fmaf(ps[hr][kk], U[k >> 1][kk >> 1][2 * hr + (kk & 1)], a);
             at[k] = a;
           }
         } else {
@@ -569,28 +615,28 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
           // ---- snapshot: merge the quad's lane states, reduce rows per op, emit partials
           float opv[kMaxOps][CPR];  // legacy packing: per-(op, class) partial (all lanes)
           if constexpr (TBL) {
-            float Mq[2], f[2], den[2];
+            float Mq[2], f[2], den[2], rden[2];
 #pragma unroll
             for (int hs = 0; hs < 2; ++hs) {
               float M = mx[hs];
               M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
               M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
-              f[hs] = mx[hs] == -CUDART_INF_F ? 0.f : ex2(mx[hs] - M);
+              f[hs] = ex2(mx[hs] - M);
               float d = sm[hs] * f[hs];
               d += __shfl_xor_sync(0xffffffffu, d, 1);
               d += __shfl_xor_sync(0xffffffffu, d, 2);
               den[hs] = d;
+              rden[hs] = __frcp_rn(d);
               Mq[hs] = M;
             }
             float accm[NSL], val[NSL];
 #pragma unroll
             for (int k = 0; k < NSL; ++k) {
-              const bool hi = (tsel >> k) & 1u;
-              float a = at[k] * (hi ? f[1] : f[0]);
+              float a = at[k] * f[k & 1];
               a += __shfl_xor_sync(0xffffffffu, a, 1);
               a += __shfl_xor_sync(0xffffffffu, a, 2);
               accm[k] = a;
-              val[k] = tgt[k] >= 0 ? __fdiv_rn(a, hi ? den[1] : den[0]) : 0.f;
+              val[k] = a * rden[k & 1];
             }
             if (walk && p.save_state && next_snap == s1 && q == 0) {
               // end of this round's extent: save the merged state for a later round to resume
@@ -607,10 +653,16 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
             }
             __syncwarp();
             float x = 0.f;
-            for (uint64_t m = red0; m; m &= m - 1) x += sv[__ffsll((long long)m) - 1];
-            for (uint64_t m = red1; m; m &= m - 1) x += sv[64 + __ffsll((long long)m) - 1];
+            if (red_n <= 4) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r)
+                if (r < red_n) x += sv[(red_off >> (8 * r)) & 255u];
+            } else {
+              for (uint64_t m = red0; m; m &= m - 1) x += sv[__ffsll((long long)m) - 1];
+              for (uint64_t m = red1; m; m &= m - 1) x += sv[64 + __ffsll((long long)m) - 1];
+            }
             __syncwarp();
-            if (red0 | red1) {
+            if (red_n > 0) {
               const int o = lane >> 3, c = lane & 7;
 #pragma unroll
               for (int v = 0; v < kMaxVar; ++v)
@@ -825,6 +877,13 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       p.tuple_done[t] = done;
     }
     }  // last
+    // advance to the next unit (the producer may already have decoded it and issued its pages)
+    if (!have_nxt) {
+      nxt = decode(u_next);
+      if (nxt.u < n_units) u_next = claim();
+    }
+    have_nxt = false;
+    cur = nxt;
   }
   if (n_cnt_rows) flush_counts(s_cnt, n_cnt_rows, p.counts);
 }

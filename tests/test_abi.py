@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "ko.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:ko_status|size_t|double|void|const char\*)\s+(ko_\w+)\(",
+    return sorted(set(re.findall(r"^\s*(?:ko_status|size_t|double|void|int32_t|const char\*)\s+(ko_\w+)\(",
                                  src, re.M)))
 
 

@@ -254,3 +254,40 @@ def test_routed_fallback_many_rows(ko):
     mg, cg = m.cpu().numpy(), c.cpu().numpy()
     parity.assert_margins(mg, m_or, mask=np.isfinite(mg))
     parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], [1, 3, 1], gold)
+
+
+@pytest.mark.parametrize("variants,plan", [
+    # rank 0 = (1000, 1) covers layer 0 entirely; (500, 2)'s layer-0 snapshot is taken in round 0
+    # and its layer-1 one in round 1 (partials persist across the rounds of the call)
+    ([(1000, 1), (500, 2)], [(0, 0, 0.25, 0.75, 0), (0, 1, 0.5, 0.5, 1)]),
+    # three nested ranks, a map and a filter fused into one read, resumed twice
+    ([(200, 1), (500, 2), (1000, 2)], [(0, 0, 0.3, 0.7, 0), (1, 0, 0.6, 0.6, 0),
+                                       (0, 1, 0.3, 0.7, 0), (1, 1, 0.5, 0.5, 1),
+                                       (0, 2, 0.5, 0.5, 1)]),
+    # the cheap stage is the later variant in plan order: ranks follow extents, not the plan
+    ([(1000, 2), (300, 1)], [(0, 1, 0.25, 0.75, 0), (0, 0, 0.5, 0.5, 1)]),
+], ids=["cross_round_partials", "three_ranks_fused_map", "ranks_by_extent"])
+def test_routed_resumable_extents(ko, variants, plan):
+    """Routed mode streams, per (tuple, layer), only the tokens past what earlier rounds read and
+    resumes their saved softmax state: every reached margin equals the oracle's."""
+    geom = Geom(2, 2, 4, 128, 1)
+    rng = np.random.default_rng(21)
+    lengths = [1, 2, 15, 16, 17, 31, 48, 64, 100, 127, 128, 129, 200, 300]
+    n_ops = 1 + max(o for (o, *_r) in plan)
+    classes = (1, 4)[:n_ops]
+    K, V, ops_h = random_problem(rng, geom, lengths, n_ops=n_ops, classes=classes)
+    pool, indptr, ids, sl = build_pool(K, V, lengths, poison=True, seed=3)
+    m_or, c_or = oracle.score(geom, pool, indptr, ids, sl, ops_h, variants)
+    # thresholds at oracle-margin quantiles so every stage sends tuples onward
+    plan = [(o, v, float(np.quantile(m_or[o, v], qlo)), float(np.quantile(m_or[o, v], qhi)), f)
+            for (o, v, qlo, qhi, f) in plan]
+    gold = np.stack([(m_or[o, -1] > 0) if classes[o] <= 1 else c_or[o, -1]
+                     for o in range(n_ops)]).astype(np.uint8)
+    kv, ops = tensors_to_device(pool, indptr, ids, sl, geom, ops_h)
+    m, c, counts = ko.score_batch(kv, ops, variants, plans=[plan], gold=torch.from_numpy(gold).cuda())
+    torch.cuda.synchronize()
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    reached = np.isfinite(mg)
+    assert reached.sum() > len(lengths)               # later rounds were reached
+    parity.assert_margins(mg, m_or, mask=reached)
+    parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], list(classes), gold)
