@@ -64,6 +64,8 @@ def lib():
         L.kg_fill_pool_device.argtypes = [ctypes.POINTER(KgCfg), ctypes.c_int64, ctypes.c_int64,
                                           P, P, P, ctypes.c_int32, P]
         L.kg_fill_pool_device.restype = ctypes.c_int
+        L.kg_read_stream.argtypes = [P, ctypes.c_int64, P, P]
+        L.kg_read_stream.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -223,3 +225,10 @@ def fill_device_pool(spec: GenSpec, t_begin: int, n_tuples: int, d_indptr: int, 
                                    int(poison), ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(f"kg_fill_pool_device failed rc={rc}")
+
+
+def read_stream(d_buf: int, nbytes: int, d_sink: int, stream: int = 0) -> None:
+    """Measurement helper (bench.py): one read-only pass over nbytes of a device buffer."""
+    if lib().kg_read_stream(ctypes.c_void_p(d_buf), int(nbytes), ctypes.c_void_p(d_sink),
+                            ctypes.c_void_p(stream)) != 0:
+        raise RuntimeError("kg_read_stream failed")

@@ -248,6 +248,61 @@ int kg_fill_pool_host(const kg_cfg* c, const int64_t* tuple_ids, int64_t n,
   return 0;
 }
 
+// Read-only HBM stream (measurement helper for bench.py's roofline context): every warp owns a
+// 3-stage shared-memory ring of 16 KiB bulk copies (cp.async.bulk + mbarrier, L2 evict-first) and
+// walks the buffer in warp-strided 16 KiB chunks, touching one word per chunk — the same
+// TMA-into-smem read path as the scoring kernel, without its math.
+__device__ __forceinline__ uint32_t rs_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+constexpr int kRsStages = 3, kRsChunk = 16384;
+__global__ void __launch_bounds__(128) read_stream_kernel(const uint8_t* __restrict__ p, int64_t n_chunks,
+                                                          uint32_t* sink) {
+  extern __shared__ __align__(128) uint8_t rs_sm[];
+  __shared__ __align__(8) uint64_t bar[4][kRsStages];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* ring = rs_sm + warp * kRsStages * kRsChunk;
+  if (lane == 0)
+    for (int s = 0; s < kRsStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rs_su32(&bar[warp][s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t nw = (int64_t)gridDim.x * 4;
+  int64_t next = (int64_t)blockIdx.x * 4 + warp, issued = 0, consumed = 0;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&]() {
+    if (lane == 0) {
+      const int s = (int)(issued % kRsStages);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(rs_su32(&bar[warp][s])),
+                   "r"(kRsChunk) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+          "[%3], %4;" ::"r"(rs_su32(ring + s * kRsChunk)), "l"(p + next * kRsChunk), "r"(kRsChunk),
+          "r"(rs_su32(&bar[warp][s])), "l"(pol) : "memory");
+    }
+    ++issued;
+    next += nw;
+  };
+  for (int k = 0; k < kRsStages && next < n_chunks; ++k) issue();
+  uint32_t acc = 0;
+  while (consumed < issued) {
+    const int s = (int)(consumed % kRsStages);
+    const uint32_t par = (uint32_t)((consumed / kRsStages) & 1);
+    uint32_t done = 0;
+    do {
+      asm volatile("{\n.reg .pred q;\nmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\nselp.u32 %0,1,0,q;\n}"
+                   : "=r"(done) : "r"(rs_su32(&bar[warp][s])), "r"(par) : "memory");
+    } while (!done);
+    acc ^= *(volatile uint32_t*)(ring + s * kRsChunk + lane * 4);
+    __syncwarp();
+    ++consumed;
+    if (next < n_chunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue();
+    }
+  }
+  if (acc == 0x9e3779b9u) sink[blockIdx.x] = acc;  // practically never taken; keeps reads live
+}
+
 // Device fill: tuples t_begin .. t_begin+n_tuples-1 with device CSR (indptr has n_tuples+1
 // entries, may start at a non-zero offset), pages written into the device pool.
 int kg_fill_pool_device(const kg_cfg* c, int64_t t_begin, int64_t n_tuples, const int64_t* d_indptr,
@@ -273,6 +328,20 @@ int kg_fill_pool_device(const kg_cfg* c, int64_t t_begin, int64_t n_tuples, cons
   cudaFree(d_rho);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 2;
+}
+
+// Measurement helper (bench.py): one read-only pass over `bytes` (multiple of 16 KiB) of a device
+// buffer through the bulk-copy ring above; its rate is the "read-stream peak" the scoring
+// kernel's achieved GB/s is compared with besides the driver's read+write copy peak.
+int kg_read_stream(const void* d_buf, int64_t bytes, uint32_t* d_sink, void* stream) {
+  const int smem = 4 * kRsStages * kRsChunk;
+  cudaFuncSetAttribute(read_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  read_stream_kernel<<<sms, 128, smem, (cudaStream_t)stream>>>((const uint8_t*)d_buf, bytes / kRsChunk,
+                                                               d_sink);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
 }  // extern "C"
