@@ -143,8 +143,6 @@ struct Workspace {
   int32_t* round_wl;              // [KO_MAX_STAGES][n_tuples] per-position worklists
   ko_plan* gplans;                // [KO_MAX_PLANS] device copy of the plans
   uint32_t* tuple_done;           // [n_tuples]
-  float* wm;                      // [n_ops][n_variants][n_tuples]
-  int32_t* wc;
   float* rstate;                  // [n_ops groups][n_tuples][n_layers][Hkv][8][rstate_w]
   int rstate_w;
   size_t rstate_group;            // floats per group slice
@@ -152,7 +150,7 @@ struct Workspace {
 };
 
 // Layout: [counters 256 B][done][part][qfrag][wfrag][tuple_state][worklist][position
-// worklists][tuple_done][wm][wc]
+// worklists][tuple_done][rstate]
 Workspace layout(const ko_kv_cache* kv, int max_cls, int max_ent, int32_t n_ops, int32_t n_variants,
                  int64_t n_work, uint8_t* base) {
   Workspace w{};
@@ -181,8 +179,6 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int max_ent, int32_t n_ops,
   w.round_wl = (int32_t*)take(sizeof(int32_t) * nt * KO_MAX_STAGES);
   w.gplans = (ko_plan*)take(sizeof(ko_plan) * KO_MAX_PLANS);
   w.tuple_done = (uint32_t*)take(sizeof(uint32_t) * nt);
-  w.wm = (float*)take(sizeof(float) * nt * n_ops * n_variants);
-  w.wc = (int32_t*)take(sizeof(int32_t) * nt * n_ops * n_variants);
   // saved softmax states of the routed rounds: a group's table needs ≤ pow2(max entries per row)
   // tiles, so 4 + 2·that floats per lane group bound every group's state
   w.rstate_w = 4 + 2 * std::min(ko::kMaxTNT, pow2_at_least(std::max(max_ent, 1)));
@@ -322,7 +318,10 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   sp.rows_per_op = kv->gqa_group * kv->n_q;
   sp.n_ops_total = n_ops_total;
   sp.n_var_total = n_var_total;
-  for (int o = 0; o < n_ops_total; ++o) sp.op_classes_g[o] = ops[o].n_classes;
+  for (int o = 0; o < n_ops_total; ++o) {
+    sp.op_classes_g[o] = ops[o].n_classes;
+    sp.bias_g[o] = ops[o].b;
+  }
   int n_l = 1;
   sp.n_var = n_vsel;
   for (int i = 0; i < KO_MAX_VARIANTS; ++i) sp.var_local[i] = -1;
@@ -656,6 +655,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     for (int k = 0; k <= r && k < n_pv; ++k) n_l = std::max(n_l, (int)variants[pv[k]].layer_cut);
     sp.n_l = n_l;
     sp.n_lh_all = kv->n_layers * kv->n_kv_heads;
+    sp.part_cpr = pow2_at_least(maxc);  // the workspace's partial class stride
     sp.avail_mask = 0;
     for (int k = 0; k < n_pv; ++k)
       if (avail[k] <= r) sp.avail_mask |= 1 << k;
@@ -692,18 +692,16 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     sp.plans[0] = P;
     sp.tuple_state = ws.tuple_state;
     sp.tuple_done = ws.tuple_done;
-    sp.wm = ws.wm;
-    sp.wc = ws.wc;
     sp.counts = (unsigned long long*)counts;
     if (g != prepped_group) {  // the fragments depend only on the group (all plan layers)
       KO_LAUNCH(ko::launch_prep(pp, s));
       prepped_group = g;
     }
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
-    KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin && pos == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
     KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, false, TNT,
                              n_work * sp.n_l * kv->n_kv_heads, s));
+    KO_LAUNCH(ko::launch_walk(sp, s));
     if (g_trace_end && pos == last_launch) KO_CUDA(cudaEventRecord(g_trace_end, s));
   }
   KO_LAUNCH(ko::launch_final_counts(rp, s));

@@ -46,6 +46,7 @@ struct ScoreParams {
   int32_t op_classes[kMaxOps];    // by local op
   int32_t op_classes_g[kMaxOps];  // by caller's op index
   const float* bias[kMaxOps];  // device fp32 [n_classes] per op
+  const float* bias_g[kMaxOps];  // same, by caller's op index (routed walk)
   int32_t rows_per_op;  // gqa * n_q
   int32_t slot_op[16];  // row slot (half*8 + g) → local op, -1 = padding
   int32_t n_ops_total, n_var_total;
@@ -85,8 +86,6 @@ struct ScoreParams {
   int32_t* wl[KO_MAX_STAGES];                 // per-position worklists
   unsigned long long* wl_len[KO_MAX_STAGES];  // their lengths (device)
   uint32_t* tuple_done;          // per tuple: 4-bit (rank + 1) computed per group, 15 = none
-  float* wm;                     // computed margins [n_ops][n_variants][n_tuples]
-  int32_t* wc;                   // computed classes
   // walk mode, resumable extents: local variants are ALL the plan's KV variants in rank order
   // (local index = rank); this launch streams, per (tuple, layer), the tokens between the
   // extent of the tuple's previous rank for this group and the extent of rank `round`, resuming
@@ -97,6 +96,7 @@ struct ScoreParams {
   float* rstate;                 // [n_tuples][n_layers][Hkv][8][rstate_w] (this group's slice)
   int32_t rstate_w;              // floats per lane group: M[2], den[2], acc[2·NT]
   int32_t n_lh_all;              // n_layers · Hkv (partials of walk mode are per tuple, all layers)
+  int32_t part_cpr;              // class stride of walk-mode partials (same for every group)
   // table-driven row/class packing (template TNT > 0): per lane group g, W·V slot k = 2·tile + hr
   // (A-row half hr) accumulates with S row g + 8·hr into the local (op, class) target
   // tgt = op·8 + class (−1: unused)
@@ -205,6 +205,8 @@ cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
 // tnt > 0: table-packed kernel with tnt W·V tiles (CPR0 = class stride of the partials)
 cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, bool nolo,
                          int tnt, int64_t max_units, cudaStream_t s);
+// routed round finaliser (margins, plan walk, counts, queueing) after a walk-mode launch_score
+cudaError_t launch_walk(const ScoreParams& p, cudaStream_t s);
 cudaError_t launch_route_reach(const RouteParams& p, cudaStream_t s);  // build worklist for stage
 cudaError_t launch_route_apply(const RouteParams& p, cudaStream_t s);  // apply stage on margins
 cudaError_t launch_route_plan(const RouteParams& p, cudaStream_t s);   // whole plan on margins

@@ -193,6 +193,79 @@ struct Ring {
   static constexpr int kSmemBytes = (kThreads / 32) * kWarpBytes + 1024;  // + alignment slack
 };
 
+// ------------------------------------------------------------------------------------------
+// Grid-mode tuple finaliser (run by the warp completing a tuple's last unit): margins/classes
+// from the partial logits, then every plan of the grid per tuple.  zs / sm_w / sc_w: this warp's
+// shared-memory scratch; s_cnt: the CTA's counters.  (Routed rounds: ko_walk_kernel.)
+// ------------------------------------------------------------------------------------------
+template <int CPR>
+__device__ __forceinline__ void finalise_tuple(const ScoreParams& p, int64_t wslot, int64_t t,
+                                               int lane, float* zs, float* sm_w, int32_t* sc_w,
+                                               int* s_cnt) {
+
+    // z = b + Σ_u partial_u over the units whose layer is inside the variant's cut, for every
+    // (op, variant, class) entry: one lane per entry sums its units in a FIXED (ascending) order in
+    // fp64, so margins stay bitwise reproducible.  This launch's partials per work slot, local
+    // (op, variant).
+    const int nz = p.n_ops * p.n_var * CPR;
+    const int n_pu = p.n_l * p.n_kv_heads;  // partial slots per tuple (layer-major)
+    const int nzg = nz;
+    const float* tpart = p.part + (size_t)wslot * n_pu * nzg;
+    for (int idx = lane; idx < nz; idx += 32) {
+      const int c = idx % CPR, ov = idx / CPR;
+      const int o = ov / p.n_var, v = ov - o * p.n_var;
+      if (c >= p.op_classes[o]) continue;
+      const float* src = tpart + idx;
+      const int nu = min(p.cut[v], p.n_layers) * p.n_kv_heads;  // l-major: l < cut ⇔ u < cut·Hkv
+      double acc = 0.0;
+      int uu = 0;
+      for (; uu + 4 <= nu; uu += 4) {
+        const float a0 = __ldcg(src + (size_t)(uu + 0) * nzg), a1 = __ldcg(src + (size_t)(uu + 1) * nzg);
+        const float a2 = __ldcg(src + (size_t)(uu + 2) * nzg), a3 = __ldcg(src + (size_t)(uu + 3) * nzg);
+        acc += (double)a0; acc += (double)a1; acc += (double)a2; acc += (double)a3;
+      }
+      for (; uu < nu; ++uu) acc += (double)__ldcg(src + (size_t)uu * nzg);
+      zs[idx] = (float)((double)__ldg(p.bias[o] + c) + acc);
+    }
+    __syncwarp();
+    for (int idx = lane; idx < p.n_ops * p.n_var; idx += 32) {
+      const int o = idx / p.n_var, v = idx % p.n_var;
+      const float* zz = zs + idx * CPR;
+      float m;
+      int cls = 0;
+      if (p.op_classes[o] <= 1) {
+        m = zz[0];
+      } else {
+        for (int c = 1; c < p.op_classes[o]; ++c)
+          if (zz[c] > zz[cls]) cls = c;  // lowest index on ties
+        float second = -CUDART_INF_F;
+        for (int c = 0; c < p.op_classes[o]; ++c)
+          if (c != cls && zz[c] > second) second = zz[c];
+        m = zz[cls] - second;
+      }
+      const size_t oi = ((size_t)p.op_ids[o] * p.n_var_total + p.var_ids[v]) * p.n_tuples + t;
+      if (p.margins) p.margins[oi] = m;
+      if (p.classes) p.classes[oi] = cls;
+      sm_w[p.op_ids[o] * p.n_var_total + p.var_ids[v]] = m;  // caller's op and variant
+      sc_w[p.op_ids[o] * p.n_var_total + p.var_ids[v]] = cls;
+    }
+    if (p.mode == MODE_GRID && p.n_ext) {
+      // external variants (margins supplied by the caller, e.g. ko_embed_scores) join the plans
+      for (int idx = lane; idx < p.n_ops_total * p.n_ext; idx += 32) {
+        const int o = idx / p.n_ext, v = p.ext_ids[idx % p.n_ext];
+        const size_t oi = ((size_t)o * p.n_var_total + v) * p.n_tuples + t;
+        sm_w[o * p.n_var_total + v] = __ldcg(p.margins + oi);
+        sc_w[o * p.n_var_total + v] = 0;
+      }
+    }
+    __syncwarp();
+    {
+      for (int gp = lane; gp < p.n_plans; gp += 32)
+        eval_plan(p.gplans[gp], sm_w, sc_w, p.n_var_total, p.op_classes_g, p.gold, p.n_tuples,
+                  t, s_cnt + gp * kCountsPerPlan);
+    }
+}
+
 // CPR0 / CPR1: classes per row slot in half 0 (A rows g) / half 1 (A rows g+8) of the row tile;
 // CPR1 = 0 when at most 8 rows attend a kv-head; partial logits are stored with stride
 // CPR = CPR0 (≥ every op's classes).  W·V tiles:
@@ -234,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   const uint32_t ring_s = smem_u32(ring);
 
   const bool walk = p.mode == MODE_WALK;
-  const int n_cnt_rows = p.mode == MODE_GRID ? p.n_plans : (p.tuple_state ? 1 : 0);  // stage/walk: row 0
+  const int n_cnt_rows = p.mode == MODE_GRID ? p.n_plans : 0;  // walk: ko_walk_kernel counts
   for (int i = threadIdx.x; i < n_cnt_rows * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&s_full[warp][s], 1);
@@ -668,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
               for (int v = 0; v < kMaxVar; ++v)
                 if (nkv[v] == next_snap)
                   p.part[((((size_t)t * p.n_lh_all + unit_lh) * p.n_ops_total + p.op_ids[o]) *
-                              p.n_var_total + p.var_ids[v]) * CPR + c] = x;
+                              p.n_var_total + p.var_ids[v]) * p.part_cpr + c] = x;
             }
           } else {
           float val[NH][CPR];
@@ -726,157 +799,26 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     }
 
    }  // heads of the unit
-    // ---- tuple completion: the warp finishing the tuple's last unit finalises it
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      // release: this unit's partial logits (stored by this lane) are visible before the count
-      uint32_t prev;
-      asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
-                   : "=r"(prev)
-                   : "l"(p.done + wslot)
-                   : "memory");
-      last = prev == (uint32_t)(upt - 1);
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
-    __threadfence();
-
-    // z = b + Σ_u partial_u over the units whose layer is inside the variant's cut, for every
-    // (op, variant, class) entry: one lane per entry sums its units in a FIXED (ascending) order in
-    // fp64, so margins stay bitwise reproducible.  Grid: this launch's partials per work slot,
-    // local (op, variant); walk: per tuple over all layers, caller's (op, variant), only the
-    // variants complete after this round (avail_mask).
-    float* zs = s_z[warp];
-    const int nz = p.n_ops * p.n_var * CPR;
-    const int n_pu = walk ? p.n_lh_all : p.n_l * Hkv;  // partial slots per tuple (layer-major)
-    const int nzg = walk ? p.n_ops_total * p.n_var_total * CPR : nz;
-    const float* tpart = p.part + (size_t)(walk ? t : wslot) * n_pu * nzg;
-    for (int idx = lane; idx < nz; idx += 32) {
-      const int c = idx % CPR, ov = idx / CPR;
-      const int o = ov / p.n_var, v = ov - o * p.n_var;
-      if (c >= p.op_classes[o] || (walk && !((p.avail_mask >> v) & 1))) continue;
-      const float* src = tpart + (walk ? (p.op_ids[o] * p.n_var_total + p.var_ids[v]) * CPR + c : idx);
-      const int nu = min(p.cut[v], p.n_layers) * Hkv;  // l-major: l < cut ⇔ u < cut·Hkv
-      double acc = 0.0;
-      int uu = 0;
-      for (; uu + 4 <= nu; uu += 4) {
-        const float a0 = __ldcg(src + (size_t)(uu + 0) * nzg), a1 = __ldcg(src + (size_t)(uu + 1) * nzg);
-        const float a2 = __ldcg(src + (size_t)(uu + 2) * nzg), a3 = __ldcg(src + (size_t)(uu + 3) * nzg);
-        acc += (double)a0; acc += (double)a1; acc += (double)a2; acc += (double)a3;
+    // ---- tuple completion (grid mode): the warp finishing the tuple's last unit finalises it;
+    // routed rounds (always table-packed) are finalised by ko_walk_kernel after the launch
+    if (!TBL && !walk) {
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        // release: this unit's partial logits (stored by this lane) are visible before the count
+        uint32_t prev;
+        asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+                     : "=r"(prev)
+                     : "l"(p.done + wslot)
+                     : "memory");
+        last = prev == (uint32_t)(upt - 1);
       }
-      for (; uu < nu; ++uu) acc += (double)__ldcg(src + (size_t)uu * nzg);
-      zs[idx] = (float)((double)__ldg(p.bias[o] + c) + acc);
-    }
-    __syncwarp();
-    for (int idx = lane; idx < p.n_ops * p.n_var; idx += 32) {
-      const int o = idx / p.n_var, v = idx % p.n_var;
-      if (walk && !((p.avail_mask >> v) & 1)) continue;
-      const float* zz = zs + idx * CPR;
-      float m;
-      int cls = 0;
-      if (p.op_classes[o] <= 1) {
-        m = zz[0];
-      } else {
-        for (int c = 1; c < p.op_classes[o]; ++c)
-          if (zz[c] > zz[cls]) cls = c;  // lowest index on ties
-        float second = -CUDART_INF_F;
-        for (int c = 0; c < p.op_classes[o]; ++c)
-          if (c != cls && zz[c] > second) second = zz[c];
-        m = zz[cls] - second;
-      }
-      const size_t oi = ((size_t)p.op_ids[o] * p.n_var_total + p.var_ids[v]) * p.n_tuples + t;
-      if (!walk) {
-        if (p.margins) p.margins[oi] = m;
-        if (p.classes) p.classes[oi] = cls;
-      } else {  // walk mode: computed margins go to the workspace; only reached ones are output
-        p.wm[oi] = m;
-        p.wc[oi] = cls;
-      }
-      s_m[warp][p.op_ids[o] * p.n_var_total + p.var_ids[v]] = m;  // caller's op and variant
-      s_c[warp][p.op_ids[o] * p.n_var_total + p.var_ids[v]] = cls;
-    }
-    if (p.mode == MODE_GRID && p.n_ext) {
-      // external variants (margins supplied by the caller, e.g. ko_embed_scores) join the plans
-      for (int idx = lane; idx < p.n_ops_total * p.n_ext; idx += 32) {
-        const int o = idx / p.n_ext, v = p.ext_ids[idx % p.n_ext];
-        const size_t oi = ((size_t)o * p.n_var_total + v) * p.n_tuples + t;
-        s_m[warp][o * p.n_var_total + v] = __ldcg(p.margins + oi);
-        s_c[warp][o * p.n_var_total + v] = 0;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        finalise_tuple<CPR>(p, wslot, t, lane, s_z[warp], s_m[warp], s_c[warp], s_cnt);
       }
     }
-    __syncwarp();
-    if (p.mode == MODE_GRID) {
-      for (int gp = lane; gp < p.n_plans; gp += 32)
-        eval_plan(p.gplans[gp], s_m[warp], s_c[warp], p.n_var_total, p.op_classes_g, p.gold, p.n_tuples,
-                  t, s_cnt + gp * kCountsPerPlan);
-    } else if (walk && lane == 0) {
-      // Routed execution: this launch is plan position `pos` = (operator group, variant rank).
-      // Walk the plan from where the tuple stopped, deciding every reached stage whose margin
-      // is available (its group was computed for this tuple at a rank ≥ the stage variant's);
-      // stop at the first one that is not and queue the tuple for the next position that
-      // computes it (Eqs. accept-i/reject-i/unsure-i; inter-op reach P:536-539).
-      const ko_plan& P = p.plans[0];
-      uint32_t state = p.pos == 0 ? 1u : p.tuple_state[t];
-      uint32_t done = p.pos == 0 ? 0xFFFFFFFFu : p.tuple_done[t];  // 4-bit rank+1 per group
-      {
-        const uint32_t cur = (done >> (4 * p.group)) & 15u;
-        const uint32_t mine = (uint32_t)p.round + 1u;
-        if (cur == 15u || cur < mine) done = (done & ~(15u << (4 * p.group))) | (mine << (4 * p.group));
-      }
-      int s = (int)((state >> kWalkStageShift) & 15u);
-      for (; s < P.n_stages; ++s) {
-        const ko_stage& st = P.stage[s];
-        const int o = st.op;
-        if (!(state & 1u) || op_status(state, o) != 0) continue;  // not reached
-        const int g = p.group_of_op[o];
-        const int rk = p.var_rank[st.variant];
-        const uint32_t have = (done >> (4 * g)) & 15u;      // 15: never computed
-        if (rk >= 0 && (have == 15u || (int)have - 1 < rk)) {  // rk < 0: external, always there
-          // the next position computing (g, ≥ rk) exists: stage s itself is one (s > pos)
-          int q = p.pos + 1;
-          while (q < p.n_pos && !(p.pos_group[q] == g && p.pos_round[q] >= rk)) ++q;
-          if (q < p.n_pos) {
-            const unsigned long long at = atomicAdd(p.wl_len[q], 1ull);
-            p.wl[q][at] = (int32_t)t;
-          }
-          break;
-        }
-        const size_t oi = ((size_t)o * p.n_var_total + st.variant) * p.n_tuples + t;
-        float m;
-        int32_t cls;
-        if (rk < 0) {                 // external variant: the caller's margin (filters only)
-          m = __ldcg(p.margins + oi);
-          cls = 0;
-        } else if (g == p.group) {
-          m = s_m[warp][o * p.n_var_total + st.variant];
-          cls = s_c[warp][o * p.n_var_total + st.variant];
-        } else {
-          m = __ldcg(p.wm + oi);
-          cls = __ldcg(p.wc + oi);
-        }
-        if (rk >= 0) {
-          if (p.margins) p.margins[oi] = m;
-          if (p.classes) p.classes[oi] = cls;
-        }
-        int* cnt = s_cnt + 5 + 4 * s;
-        atomicAdd(&cnt[0], 1);
-        const int d = decide(m, st, p.op_classes_g[o]);
-        if (d == D_ACCEPT || d == D_RESOLVED) {
-          state |= 1u << (1 + 2 * o);
-          if (d == D_RESOLVED) state |= ((uint32_t)cls & 15u) << (16 + 4 * o);
-          atomicAdd(&cnt[1], 1);
-        } else if (d == D_REJECT) {
-          state = (state & ~1u) | (2u << (1 + 2 * o));
-          atomicAdd(&cnt[2], 1);
-        } else {
-          atomicAdd(&cnt[3], 1);
-        }
-      }
-      p.tuple_state[t] = (state & ~(15u << kWalkStageShift)) | ((uint32_t)s << kWalkStageShift);
-      p.tuple_done[t] = done;
-    }
-    }  // last
     // advance to the next unit (the producer may already have decoded it and issued its pages)
     if (!have_nxt) {
       nxt = decode(u_next);
@@ -1184,6 +1126,131 @@ int num_sms() {
   return n;
 }
 
+// Routed round finaliser (after each walk-mode scoring launch): ONE THREAD PER TUPLE of the round
+// walks the plan from where the tuple stopped (Eqs. accept-i/reject-i/unsure-i, P:323-327;
+// inter-op reach P:536-539), deciding every reached stage whose margin is available — computed on
+// demand from the per-tuple partial logits (z_c = b_c + Σ_u partial, fp64, u ascending: the grid
+// finaliser's arithmetic) and written out, since only reached entries are outputs (§8(b)) — and
+// stops at the first stage whose margin is not yet available, queueing the tuple for the first
+// LATER plan position that computes it.  Per-stage counts: shared-memory atomics flushed once per
+// CTA; queue appends are warp-aggregated.
+__device__ __forceinline__ float walk_margin(const ScoreParams& p, int64_t t, int o, int v,
+                                             int32_t* cls_out) {
+  const int CPR = p.part_cpr;  // one class stride for every group's partials
+  const int nzg = p.n_ops_total * p.n_var_total * CPR;
+  const int nu = min(p.cut[p.var_local[v]], p.n_layers) * p.n_kv_heads;  // l-major units
+  const float* src = p.part + (size_t)t * p.n_lh_all * nzg + (size_t)(o * p.n_var_total + v) * CPR;
+  const int C = p.op_classes_g[o];
+  float best = -CUDART_INF_F, second = -CUDART_INF_F;
+  int bi = 0;
+  for (int c = 0; c < C; ++c) {
+    double acc = 0.0;
+    int u = 0;
+    for (; u + 4 <= nu; u += 4) {
+      const float a0 = __ldcg(src + (size_t)(u + 0) * nzg + c), a1 = __ldcg(src + (size_t)(u + 1) * nzg + c);
+      const float a2 = __ldcg(src + (size_t)(u + 2) * nzg + c), a3 = __ldcg(src + (size_t)(u + 3) * nzg + c);
+      acc += (double)a0; acc += (double)a1; acc += (double)a2; acc += (double)a3;
+    }
+    for (; u < nu; ++u) acc += (double)__ldcg(src + (size_t)u * nzg + c);
+    const float z = (float)((double)__ldg(p.bias_g[o] + c) + acc);
+    if (C <= 1) {
+      *cls_out = 0;
+      return z;
+    }
+    if (z > best) {  // lowest class index on ties
+      second = best;
+      best = z;
+      bi = c;
+    } else if (z > second) {
+      second = z;
+    }
+  }
+  *cls_out = bi;
+  return best - second;
+}
+
+constexpr int kWalkThreads = 256;
+__global__ void __launch_bounds__(kWalkThreads) ko_walk_kernel(const __grid_constant__ ScoreParams p) {
+  __shared__ int s_cnt[4 * KO_MAX_STAGES];
+  for (int i = threadIdx.x; i < 4 * KO_MAX_STAGES; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t n_work = p.work_len_dev ? *p.work_len_dev : p.work_len_host;
+  const ko_plan& P = p.plans[0];
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_work;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = base + threadIdx.x;
+    int qdest = -1;
+    int64_t t = 0;
+    if (w < n_work) {
+      t = p.work ? (int64_t)p.work[w] : w;
+      uint32_t state = p.pos == 0 ? 1u : __ldcg(p.tuple_state + t);
+      uint32_t done = p.pos == 0 ? 0xFFFFFFFFu : __ldcg(p.tuple_done + t);  // 4-bit round+1 per group
+      {
+        const uint32_t cur = (done >> (4 * p.group)) & 15u;
+        const uint32_t mine = (uint32_t)p.round + 1u;
+        if (cur == 15u || cur < mine) done = (done & ~(15u << (4 * p.group))) | (mine << (4 * p.group));
+      }
+      const int s_from = (int)((state >> kWalkStageShift) & 15u);
+      int stop = P.n_stages;
+      for (int s = s_from; s < P.n_stages; ++s) {
+        const ko_stage& st = P.stage[s];
+        const int o = st.op;
+        if (!(state & 1u) || op_status(state, o) != 0) continue;  // not reached
+        const int g = p.group_of_op[o];
+        const int rk = p.var_rank[st.variant];
+        const uint32_t have = (done >> (4 * g)) & 15u;      // 15: never computed
+        if (rk >= 0 && (have == 15u || (int)have - 1 < rk)) {  // rk < 0: external, always there
+          // the next position computing (g, ≥ rk) exists: stage s itself is one (s > pos)
+          int q = p.pos + 1;
+          while (q < p.n_pos && !(p.pos_group[q] == g && p.pos_round[q] >= rk)) ++q;
+          if (q < p.n_pos) qdest = q;
+          stop = s;
+          break;
+        }
+        const size_t oi = ((size_t)o * p.n_var_total + st.variant) * p.n_tuples + t;
+        float m;
+        int32_t cls = 0;
+        if (rk < 0) {                 // external variant: the caller's margin (filters only)
+          m = __ldcg(p.margins + oi);
+        } else {
+          m = walk_margin(p, t, o, st.variant, &cls);
+          if (p.margins) p.margins[oi] = m;
+          if (p.classes) p.classes[oi] = cls;
+        }
+        const int d = decide(m, st, p.op_classes_g[o]);
+        int k = 3;  // [n_in, n_acc, n_rej, n_uns] of stage s
+        if (d == D_ACCEPT || d == D_RESOLVED) {
+          state |= 1u << (1 + 2 * o);
+          if (d == D_RESOLVED) state |= ((uint32_t)cls & 15u) << (16 + 4 * o);
+          k = 1;
+        } else if (d == D_REJECT) {
+          state = (state & ~1u) | (2u << (1 + 2 * o));
+          k = 2;
+        }
+        atomicAdd(&s_cnt[4 * s], 1);
+        atomicAdd(&s_cnt[4 * s + k], 1);
+      }
+      p.tuple_state[t] = (state & ~(15u << kWalkStageShift)) | ((uint32_t)stop << kWalkStageShift);
+      p.tuple_done[t] = done;
+    }
+    // warp-aggregated queue appends: lanes with the same destination share one atomic
+    const unsigned act = __ballot_sync(0xffffffffu, qdest >= 0);
+    if (qdest >= 0) {
+      const unsigned same = __match_any_sync(act, qdest);
+      const int leader = __ffs(same) - 1;
+      unsigned long long at = 0;
+      if (lane == leader) at = atomicAdd(p.wl_len[qdest], (unsigned long long)__popc(same));
+      at = __shfl_sync(same, at, leader);
+      p.wl[qdest][at + __popc(same & ((1u << lane) - 1u))] = (int32_t)t;
+    }
+  }
+  // per-stage counts: shared-memory atomics per CTA, one global atomic per counter per CTA
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * KO_MAX_STAGES; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(&p.counts[5 + i], (unsigned long long)s_cnt[i]);
+}
+
 template <int D, int CPR0, int CPR1, bool NOLO, int TNT>
 cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t s) {
   static int occ = 0;
@@ -1337,6 +1404,12 @@ cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1,
 #undef KO_DISPATCH_NOLO
 #undef KO_DISPATCH
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_walk(const ScoreParams& p, cudaStream_t s) {
+  // grid-stride over the round's work list (its length is on the device)
+  ko_walk_kernel<<<num_sms() * 4, kWalkThreads, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_route_init(uint32_t* state, int64_t n, cudaStream_t s) {
