@@ -268,8 +268,21 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     wl = workloads.get(args.config)
-    n = args.n_tuples or wl.bench_n or wl.n_tuples
-    t0 = rank * n                   # weak scaling: rank r owns tuple ids r·n .. r·n + n − 1
+    n_per = args.n_tuples or wl.bench_n or wl.n_tuples
+    # weak scaling: the dataset is world·n_per tuples; rank r owns a contiguous range — r·n_per
+    # .. r·n_per + n_per − 1, or for variable lengths the range balanced by algorithmic bytes
+    # (full-read upper bound per tuple)
+    t0, n = rank * n_per, n_per
+    if world > 1 and wl.spec.len_min != wl.spec.len_max:
+        from paper_2602_04430_b200.dist import shard_by_cost
+        sl_all = wl.spec.seq_len(0, world * n_per).astype(np.int64)
+        cost = np.zeros(len(sl_all))
+        for l in range(wl.spec.n_layers):
+            ks = [k for (k, c) in wl.variants if c > l]
+            if ks:
+                cost += n_kept(sl_all, max(ks))
+        t0, t1 = shard_by_cost(cost, rank, world)
+        n = t1 - t0
     d = device_workload(wl, t0=t0, n=n, placement="contiguous")
     kv, ops, gold = d["kv"], d["ops"], d["gold"]
     n_var, n_ops = len(wl.variants), wl.spec.n_ops
@@ -317,7 +330,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = world * n * args.steps / (ms_total / 1000.0)
+    value = world * n_per * args.steps / (ms_total / 1000.0)   # every rank's tuples
 
     cnt = counts.cpu().numpy()
     routed = len(plans) == 1
@@ -344,7 +357,7 @@ def main():
         best, _ = plan_select.select_plan(plans, cnt, wl.variants, target_recall=0.9)
         selection = {"target_recall": 0.9, "alpha": 0.95,
                      "plan": None if best is None else best.index,
-                     "cost_vs_gold": None if best is None else best.cost / (world * n * wl.spec.n_ops),
+                     "cost_vs_gold": None if best is None else best.cost / (world * n_per * wl.spec.n_ops),
                      "recall_lb": None if best is None else best.recall_lb}
 
     cb = None
@@ -528,10 +541,14 @@ def run_e2e(args, ko, torch, wl, d, ops, gold, plans, margins, classes, counts, 
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    n_all = torch.tensor([n], dtype=torch.int64, device="cuda")   # tuples of every rank's batch
+    if dist is not None:
+        dist.all_reduce(n_all, op=dist.ReduceOp.SUM)
+    n_all = int(n_all.item())
     h2d = n_pages * page_bytes
     d2h = h_counts.numel() * 8 + h_margins.numel() * 4
     del host_pool
-    return {"value": world * n * args.e2e_steps / (ms / 1000.0), "unit": UNIT,
+    return {"value": n_all * args.e2e_steps / (ms / 1000.0), "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
             "ms_per_step": ms / args.e2e_steps, "tuples_per_rank": n,
             "how": "pinned host KV pages -> device in 8 tuple chunks on a copy stream, "

@@ -16,6 +16,32 @@ def shard_range(n_total: int, rank: int, world: int) -> Tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
+def shard_by_cost(costs, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous tuple range [begin, end) of `rank` balanced by per-tuple cost (SURVEY §8(e):
+    algorithmic bytes, the full-read upper bound Σ_l Hkv·4·d·need(t, l) — it matters for variable
+    lengths).  Rank r's range ends at the first tuple whose inclusive cost prefix reaches
+    (r + 1)/world of the total, so every boundary is within one tuple's cost of the ideal split;
+    the ranges are contiguous, disjoint and cover every tuple."""
+    import numpy as np
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    c = np.asarray(costs, dtype=np.float64)
+    if c.ndim != 1 or (c < 0).any():
+        raise ValueError("costs must be a non-negative vector")
+    n = len(c)
+    pre = np.cumsum(c)
+    total = pre[-1] if n else 0.0
+
+    def cut(k):
+        if k <= 0:
+            return 0
+        if k >= world or total == 0:
+            return n if k >= world else (n * k) // world
+        return int(np.searchsorted(pre, total * k / world, side="left")) + 1
+
+    return min(cut(rank), n), min(cut(rank + 1), n)
+
+
 def weak_shard(n_per_rank: int, rank: int) -> Tuple[int, int]:
     """Weak scaling: rank r owns tuple ids r·n .. r·n + n − 1 of an N·n-tuple dataset."""
     return rank * n_per_rank, (rank + 1) * n_per_rank

@@ -73,3 +73,22 @@ def test_shard_range_partitions(n, world):
         seen += list(range(b, e))
         assert e - b in (n // world, n // world + 1)
     assert seen == list(range(n))
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_by_cost_contiguous_cover_and_balanced(world):
+    """Byte-balanced sharding: contiguous, disjoint, covering ranges whose costs
+    differ from the ideal share by at most one tuple's cost (log-uniform C3-like lengths)."""
+    rng = np.random.default_rng(world)
+    L = np.exp(rng.uniform(np.log(256), np.log(4096), size=5000)).astype(np.int64)
+    cost = L * 2 * 8 * 4 * 128.0                     # bytes: layers · heads · (K+V, bf16) · d
+    ranges = [kodist.shard_by_cost(cost, r, world) for r in range(world)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == len(cost)
+    for (a, b), (c, d) in zip(ranges, ranges[1:]):
+        assert b == c and a <= b
+    share = cost.sum() / world
+    for a, b in ranges:
+        assert abs(cost[a:b].sum() - share) <= 2 * cost.max()
+    # equal costs reduce to an equal split
+    eq = [kodist.shard_by_cost(np.ones(12), r, 4) for r in range(4)]
+    assert eq == [(0, 3), (3, 6), (6, 9), (9, 12)]
