@@ -58,6 +58,23 @@ def n_kept(L, keep):
     return np.maximum(1, (L.astype(np.int64) * keep) // 1000)
 
 
+def rank_range(wl, n_per, rank, world):
+    """(first tuple id, tuple count) of this rank under weak scaling: the dataset is world·n_per
+    tuples; fixed lengths → ids r·n_per .. r·n_per + n_per − 1; variable lengths → the contiguous
+    range balanced by algorithmic bytes (full-read upper bound per tuple)."""
+    if world == 1 or wl.spec.len_min == wl.spec.len_max:
+        return rank * n_per, n_per
+    from paper_2602_04430_b200.dist import shard_by_cost
+    sl_all = wl.spec.seq_len(0, world * n_per).astype(np.int64)
+    cost = np.zeros(len(sl_all))
+    for l in range(wl.spec.n_layers):
+        ks = [k for (k, c) in wl.variants if c > l]
+        if ks:
+            cost += n_kept(sl_all, max(ks))
+    t0, t1 = shard_by_cost(cost, rank, world)
+    return t0, t1 - t0
+
+
 def algorithmic_bytes_routed(wl, seq_len, margins):
     """Routed mode: need(t,l) = largest n_kept over the (op, variant) entries the GPU itself
     reached for tuple t (finite margins, §8(d)) whose layer cut includes l."""
@@ -272,17 +289,7 @@ def main():
     # weak scaling: the dataset is world·n_per tuples; rank r owns a contiguous range — r·n_per
     # .. r·n_per + n_per − 1, or for variable lengths the range balanced by algorithmic bytes
     # (full-read upper bound per tuple)
-    t0, n = rank * n_per, n_per
-    if world > 1 and wl.spec.len_min != wl.spec.len_max:
-        from paper_2602_04430_b200.dist import shard_by_cost
-        sl_all = wl.spec.seq_len(0, world * n_per).astype(np.int64)
-        cost = np.zeros(len(sl_all))
-        for l in range(wl.spec.n_layers):
-            ks = [k for (k, c) in wl.variants if c > l]
-            if ks:
-                cost += n_kept(sl_all, max(ks))
-        t0, t1 = shard_by_cost(cost, rank, world)
-        n = t1 - t0
+    t0, n = rank_range(wl, n_per, rank, world)
     d = device_workload(wl, t0=t0, n=n, placement="contiguous")
     kv, ops, gold = d["kv"], d["ops"], d["gold"]
     n_var, n_ops = len(wl.variants), wl.spec.n_ops
