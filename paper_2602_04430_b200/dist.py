@@ -55,6 +55,13 @@ def combine_counts(counts, group=None):
     return counts
 
 
+def combine_soft(out, group=None):
+    """In-place all-reduce(SUM) of a ko_soft_stats fp64 output vector across ranks: the relaxed
+    TP/FP/FN/cost and every Jacobian entry are sums over tuples, so each rank
+    evaluates its own tuple shard and one all-reduce per optimizer iteration combines them."""
+    return combine_counts(out, group)
+
+
 def max_over_ranks(value: float, device=None, group=None) -> float:
     """Max of a per-rank scalar (device time) over the group — the timing rule of bench.py."""
     import torch

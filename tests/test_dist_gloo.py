@@ -92,3 +92,40 @@ def test_shard_by_cost_contiguous_cover_and_balanced(world):
     # equal costs reduce to an equal split
     eq = [kodist.shard_by_cost(np.ones(12), r, 4) for r in range(4)]
     assert eq == [(0, 3), (3, 6), (6, 9), (9, 12)]
+
+
+def _soft_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import soft
+    rng = np.random.default_rng(5)
+    n = 701
+    m = torch.from_numpy(rng.normal(0, 2, size=(2, 2, n)))
+    gold = torch.from_numpy((rng.random((2, n)) < 0.4).astype(np.float64))
+    plan = [(0, 0, -0.5, 0.5, 0), (0, 1, 0.0, 0.0, 1), (1, 0, -1.0, 1.0, 0), (1, 1, 0.0, 0.0, 1)]
+    s = torch.tensor([0.3, 0.0, -0.2, 0.0], dtype=torch.float64)
+    lo = torch.tensor([st[2] for st in plan], dtype=torch.float64)
+    hi = torch.tensor([st[3] for st in plan], dtype=torch.float64)
+    cost = torch.tensor([1.0, 4.0, 1.0, 4.0], dtype=torch.float64)
+    b, e = kodist.shard_range(n, rank, world)
+    part = torch.stack(list(soft.soft_forward(plan, s, lo, hi, 0.5, m[:, :, b:e], gold[:, b:e], cost)))
+    kodist.combine_soft(part)
+    full = torch.stack(list(soft.soft_forward(plan, s, lo, hi, 0.5, m, gold, cost)))
+    if rank == 0:
+        out.put((part.numpy().tolist(), full.numpy().tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_soft_relaxation_sums_equal_single_rank():
+    """NEXT-1 sharded: per-rank relaxed TP/FP/FN/cost all-reduced over gloo = the 1-rank values."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_soft_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    part, full = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    assert np.allclose(part, full, rtol=1e-12, atol=1e-9)

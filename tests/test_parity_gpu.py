@@ -291,3 +291,28 @@ def test_routed_resumable_extents(ko, variants, plan):
     assert reached.sum() > len(lengths)               # later rounds were reached
     parity.assert_margins(mg, m_or, mask=reached)
     parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], list(classes), gold)
+
+
+def test_routed_subset_and_launch_count(ko):
+    """Routed mode on a tuple subset (tuple_idx): only subset tuples are scored (the rest stay
+    NaN) and the counts equal the oracle's on the subset; ko_last_launch_count reports the
+    library's launches (prep once per group, score + walk per launched position, final counts)."""
+    wl = workloads.get("C4")
+    n = 3000
+    d = device_workload(wl, n=n)
+    plan = wl.plans[0]
+    sub = np.arange(7, n, 5, dtype=np.int32)
+    m, c, counts = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan], gold=d["gold"],
+                                  tuple_idx=torch.from_numpy(sub).cuda())
+    torch.cuda.synchronize()
+    launches = ko.last_launch_count()
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    outside = np.setdiff1d(np.arange(n), sub)
+    assert np.isnan(mg[:, :, outside]).all()
+    m_or, c_or = oracle.score_workload(wl, np.arange(n))
+    gold = d["gold"].cpu().numpy()
+    parity.assert_margins(mg[:, :, sub], m_or[:, :, sub], mask=np.isfinite(mg[:, :, sub]))
+    parity.assert_counts(counts.cpu().numpy(), m_or[:, :, sub], c_or[:, :, sub], mg[:, :, sub],
+                         cg[:, :, sub], [plan], wl.spec.op_classes, gold[:, sub])
+    # C4's plan: one fused group; positions 0, 1, 3, 5 launched (2 and 4 are covered by 0)
+    assert launches == 1 + 2 * 4 + 1
