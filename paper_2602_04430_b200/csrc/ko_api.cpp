@@ -490,11 +490,30 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
       if (is_external(variants[i])) ext[n_ext++] = i; else var_sel[n_int++] = i;
     }
     if (n_int == 0) return fail(KO_EINVAL, "no KV variant to score (all variants external)");
-    int CPR0 = 1, CPR1 = 0;
+    int CPR0 = 1, CPR1 = 0, TNT = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
     fill_common(sp, pp, kv, ops, op_sel, n_ops, variants, var_sel, n_int, n_ops, n_variants,
                 ws, &CPR0, &CPR1);
+    {
+      // the table packing when it needs fewer W·V tiles than the half/class layout (a K-class map
+      // beside filters: 2 tiles instead of 3, W fragments in registers)
+      const int nt_legacy = pp.nolo ? (CPR0 + 1) / 2 + (CPR1 + 1) / 2 : CPR0 + CPR1;
+      ko::ScoreParams tsp;
+      ko::PrepParams tpp;
+      int tc0 = 1, tc1 = 0, tnt = 0;
+      if (nt_legacy >= 3) {
+        fill_common(tsp, tpp, kv, ops, op_sel, n_ops, variants, var_sel, n_int, n_ops, n_variants,
+                    ws, &tc0, &tc1, &tnt);
+        if (tnt > 0 && tnt < nt_legacy) {
+          sp = tsp;
+          pp = tpp;
+          CPR0 = tc0;
+          CPR1 = 0;
+          TNT = tnt;
+        }
+      }
+    }
     sp.n_ext = n_ext;
     for (int i = 0; i < n_ext; ++i) sp.ext_ids[i] = ext[i];
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
@@ -516,7 +535,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0, 0,
+    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0, TNT,
                              n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end) KO_CUDA(cudaEventRecord(g_trace_end, s));
     return KO_OK;

@@ -739,9 +739,16 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
               const int o = lane >> 3, c = lane & 7;
 #pragma unroll
               for (int v = 0; v < kMaxVar; ++v)
-                if (nkv[v] == next_snap)
-                  p.part[((((size_t)t * p.n_lh_all + unit_lh) * p.n_ops_total + p.op_ids[o]) *
-                              p.n_var_total + p.var_ids[v]) * p.part_cpr + c] = x;
+                if (nkv[v] == next_snap) {
+                  // walk: per tuple (persisting across rounds), caller's (op, variant); grid: per
+                  // work slot, local (op, variant) — the grid finaliser's layout
+                  const size_t at =
+                      walk ? ((((size_t)t * p.n_lh_all + unit_lh) * p.n_ops_total + p.op_ids[o]) *
+                                  p.n_var_total + p.var_ids[v]) * p.part_cpr + c
+                           : ((((size_t)wslot * p.n_l * Hkv + unit_lh) * p.n_ops + o) * p.n_var + v) *
+                                 CPR + c;
+                  p.part[at] = x;
+                }
             }
           } else {
           float val[NH][CPR];
@@ -800,8 +807,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 
    }  // heads of the unit
     // ---- tuple completion (grid mode): the warp finishing the tuple's last unit finalises it;
-    // routed rounds (always table-packed) are finalised by ko_walk_kernel after the launch
-    if (!TBL && !walk) {
+    // routed rounds are finalised by ko_walk_kernel after the launch
+    if (!walk) {
       __syncwarp();
       int last = 0;
       if (lane == 0) {
