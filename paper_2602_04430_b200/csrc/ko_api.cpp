@@ -502,7 +502,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
       ko::ScoreParams tsp;
       ko::PrepParams tpp;
       int tc0 = 1, tc1 = 0, tnt = 0;
-      if (nt_legacy >= 3) {
+      if (nt_legacy >= 2) {
         fill_common(tsp, tpp, kv, ops, op_sel, n_ops, variants, var_sel, n_int, n_ops, n_variants,
                     ws, &tc0, &tc1, &tnt);
         if (tnt > 0 && tnt < nt_legacy) {
