@@ -467,7 +467,7 @@ def run_next(args):
                 "config": {"workload": f"C2 geometry, {n} tuples x 512 tokens, {kvb} B of KV"}}
     else:
         wl = workloads.get("C5")
-        n = args.n_tuples or 1_000_000
+        n = args.n_tuples or 8_000_000      # 4.1 GB of item embeddings: steady-state rate
         dim = 256
         item, op = wl.spec.embeddings(0, n, dim)
         di = torch.from_numpy(item.view(np.int16)).cuda().view(torch.bfloat16)

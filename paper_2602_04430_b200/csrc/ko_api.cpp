@@ -847,6 +847,32 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
   ep.n_idx = n_idx;
   ep.margins = margins;
   if ((tuple_idx ? n_idx : n_tuples) == 0) return KO_OK;
+  ep.use_tmap = 0;
+  static const int emb_tmap = [] {  // A/B knob: 2-D tensor-map loads for contiguous rows
+    const char* e = std::getenv("KO_EMB_TMAP");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (emb_tmap && !tuple_idx && dim % 16 == 0 && dim <= 512 && n_tuples > 0 && n_tuples < (1ll << 31)) {
+    // contiguous rows: a 2-D tensor map (box 64 dims × 16 rows, 128B swizzle) over item_emb
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult qr;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+          qr == cudaDriverEntryPointSuccess)
+        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    if (encode) {
+      cuuint64_t dims[2] = {(cuuint64_t)dim, (cuuint64_t)n_tuples};
+      cuuint64_t strides[1] = {(cuuint64_t)dim * 2};
+      cuuint32_t box[2] = {64, 16};
+      cuuint32_t estr[2] = {1, 1};
+      if (encode(&ep.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(item_emb), dims,
+                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        ep.use_tmap = 1;
+    }
+  }
   KO_LAUNCH(ko::launch_embed(ep, (cudaStream_t)stream));
   return KO_OK;
 }

@@ -156,6 +156,8 @@ struct ReduceParams {
 
 // embedding-similarity stage
 struct EmbedParams {
+  alignas(64) CUtensorMap tmap;  // item_emb as 2-D bf16 [n_tuples][dim], box 64 × 16, 128B swizzle
+  int32_t use_tmap;              // contiguous rows (tuple_idx == NULL): tensor-map loads
   const uint16_t* item_emb;  // bf16 [n_tuples][dim]
   const uint16_t* op_emb;    // bf16 [n_e][dim]
   int32_t dim, n_e;

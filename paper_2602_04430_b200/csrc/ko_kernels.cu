@@ -1363,10 +1363,225 @@ __global__ void __launch_bounds__(256) embed_kernel(const __grid_constant__ Embe
   }
 }
 
+// Tensor-core path (dim a multiple of 16, ≤ 512): per warp a 3-stage shared-memory ring of
+// 16-tuple blocks, each item row brought in by its own 1-D bulk copy (cp.async.bulk, one lane per
+// row, tuple_idx gathers for free) into a row padded by 16 B so ldmatrix is conflict-free.  Per
+// k-step of 16 dims one ldmatrix.x4 gives the A fragment X[16 tuples × 16 dims]; then
+//   D = X · Qᵀ  (B = the ≤ 4 operator embeddings, fragments in registers)   — the dot products,
+//   G = X · Xᵀ  (B = the A fragment itself: rows 0-7 = {a0, a2}, rows 8-15 = {a1, a3})
+// whose diagonal holds the squared norms; fp32 accumulation (mma.sync m16n8k16 bf16).  The
+// epilogue takes the diagonal (lane (g, g/2) holds ‖x_g‖² and ‖x_{g+8}‖²) and writes the cosines.
+#ifndef KO_EMB_STAGES
+#define KO_EMB_STAGES 3
+#endif
+constexpr int kEmbWarps = 4, kEmbStages = KO_EMB_STAGES, kEmbRows = 16;
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816b(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                          uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+               "{%8,%9}, {%0,%1,%2,%3};\n"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int KSM, bool TM>  // k-steps of 16 dims (dim ≤ 16·KSM); TM: tensor-map loads
+__global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_constant__ EmbedParams p) {
+  extern __shared__ __align__(128) uint8_t emb_sm[];
+  __shared__ __align__(8) uint64_t bar[kEmbWarps][kEmbStages];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int dim = p.dim, KS = dim / 16;
+  // row layout of a stage: TM — NB boxes of 16 rows × 128 B (64 dims), 128B-swizzled; else rows
+  // padded to dim·2 + 16 bytes (each row its own bulk copy)
+  const int NB = (dim + 63) / 64;
+  const int RS = dim * 2 + 16;                        // padded row stride (bytes), !TM
+  const int SB = TM ? NB * kEmbRows * 128 : kEmbRows * RS;  // stage bytes
+  uint8_t* base = TM ? reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(emb_sm) + 1023) &
+                                                  ~static_cast<uintptr_t>(1023))  // swizzle atom
+                     : emb_sm;
+  uint8_t* ring = base + (size_t)warp * kEmbStages * SB;
+  const uint32_t ring_s = smem_u32(ring);
+  if (lane == 0) {
+    for (int s = 0; s < kEmbStages; ++s) mbar_init(&bar[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // operator embeddings as B fragments: lane (g, q) holds op g's dims 16·ks + {2q, 2q+1} and
+  // 16·ks + 8 + {2q, 2q+1} (zero for g ≥ n_e); and each op's norm
+  uint32_t bq[KSM][2];
+#pragma unroll
+  for (int ks = 0; ks < KSM; ++ks) {
+    bq[ks][0] = bq[ks][1] = 0u;
+    if (ks < KS && g < p.n_e) {
+      const uint16_t* e = p.op_emb + (size_t)g * dim + 16 * ks + 2 * q;
+      bq[ks][0] = (uint32_t)e[0] | ((uint32_t)e[1] << 16);
+      bq[ks][1] = (uint32_t)e[8] | ((uint32_t)e[9] << 16);
+    }
+  }
+  float qn[KO_MAX_OPS];
+#pragma unroll
+  for (int o = 0; o < KO_MAX_OPS; ++o) {
+    float acc = 0.f;
+    if (o < p.n_e)
+      for (int d = lane; d < dim; d += 32) {
+        const float x = __bfloat162float(__ushort_as_bfloat16(p.op_emb[(size_t)o * dim + d]));
+        acc = fmaf(x, x, acc);
+      }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    qn[o] = sqrtf(acc);
+  }
+  // this lane's outputs: ops 2q and 2q + 1 (C fragment columns) — row pointer and 1/‖q‖
+  float* out[2];
+  float rq[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int o = 2 * q + e;
+    float qo = qn[0];
+#pragma unroll
+    for (int o2 = 1; o2 < KO_MAX_OPS; ++o2)
+      if (o == o2) qo = qn[o2];
+    out[e] = o < p.n_e ? p.margins + ((size_t)p.op_ids[o] * p.n_variants + p.variant) * p.n_tuples
+                       : nullptr;
+    rq[e] = qo > 0.f ? 1.f / qo : 0.f;
+  }
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+
+  const int64_t n = p.tuple_idx ? p.n_idx : p.n_tuples;
+  const int64_t n_blk = (n + kEmbRows - 1) / kEmbRows;
+  const int64_t nw = (int64_t)gridDim.x * kEmbWarps;
+  int64_t next = (int64_t)blockIdx.x * kEmbWarps + warp;  // next block to issue
+  uint32_t issued = 0, consumed = 0;
+  const uint32_t row_bytes = (uint32_t)dim * 2;
+  auto tuple_of = [&](int64_t w) -> int64_t { return p.tuple_idx ? (int64_t)p.tuple_idx[w] : w; };
+  auto issue = [&]() {
+    const int slot = issued % kEmbStages;
+    const int64_t w0 = next * kEmbRows;
+    const int rows = (int)(n - w0 < kEmbRows ? n - w0 : kEmbRows);
+    if constexpr (TM) {  // NB boxes (64 dims × 16 rows); out-of-range rows / dims are zero-filled
+      if (lane == 0) {
+        mbar_expect_tx(&bar[warp][slot], (uint32_t)SB);
+        for (int b = 0; b < NB; ++b)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(ring_s + slot * SB + b * kEmbRows * 128),
+              "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(64 * b), "r"((int)w0),
+              "r"(smem_u32(&bar[warp][slot])), "l"(policy)
+              : "memory");
+      }
+      ++issued;
+      next += nw;
+      return;
+    }
+    // gathered rows: one 1-D bulk copy per row, all issued by lane 0 (a bulk copy takes uniform
+    // operands; lanes issuing their own rows would be serialised by the compiler anyway)
+    const int64_t tl = lane < rows ? tuple_of(w0 + lane) : 0;
+    if (lane == 0) mbar_expect_tx(&bar[warp][slot], row_bytes * rows);
+    for (int r = 0; r < rows; ++r) {
+      const int64_t t = __shfl_sync(0xffffffffu, tl, r);
+      if (lane == 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+            "%2, [%3], %4;" ::"r"(ring_s + slot * SB + r * RS),
+            "l"(p.item_emb + (size_t)t * dim), "r"(row_bytes), "r"(smem_u32(&bar[warp][slot])),
+            "l"(policy)
+            : "memory");
+    }
+    ++issued;
+    next += nw;
+  };
+  for (int k = 0; k < kEmbStages && next < n_blk; ++k) issue();
+  // ldmatrix row address of this lane inside a stage: matrix (lane / 8) = (rows +8·(m&1),
+  // dims +8·(m>>1)); row (lane & 7)
+  const uint32_t lrow = (uint32_t)((lane & 7) + 8 * ((lane >> 3) & 1)) * RS + 16 * (lane >> 4);
+  for (int64_t blk = (int64_t)blockIdx.x * kEmbWarps + warp; blk < n_blk; blk += nw) {
+    const int slot = consumed % kEmbStages;
+    mbar_wait(&bar[warp][slot], (consumed / kEmbStages) & 1u);
+    const uint32_t st = ring_s + slot * SB + (TM ? 0u : lrow);
+    // two accumulator sets (even / odd k-steps) halve the MMA dependency chains
+    float dd[2][4] = {}, g0[2][4] = {}, g1[2][4] = {};
+#pragma unroll
+    for (int ks = 0; ks < KSM; ++ks) {
+      if (ks < KS) {
+        uint32_t a[4];
+        if constexpr (TM) {
+          // box ks/4, 16-byte chunk 2·(ks%4) + (matrix ≥ 2), XORed with the row (128B swizzle)
+          const int r = (lane & 7) + 8 * ((lane >> 3) & 1);
+          const int c = 2 * (ks & 3) + (lane >> 4);
+          ldsm_x4(a, st + (ks >> 2) * (kEmbRows * 128) + r * 128 + ((c ^ (r & 7)) << 4));
+        } else {
+          ldsm_x4(a, st + 32 * ks);
+        }
+        mma16816b(dd[ks & 1], a, bq[ks][0], bq[ks][1]);
+        mma16816b(g0[ks & 1], a, a[0], a[2]);
+        mma16816b(g1[ks & 1], a, a[1], a[3]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      dd[0][i] += dd[1][i];
+      g0[0][i] += g0[1][i];
+      g1[0][i] += g1[1][i];
+    }
+    __syncwarp();
+    ++consumed;
+    if (next < n_blk) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue();
+    }
+    // squared norms of tuples g and g + 8 sit in lane (g, g/2): G0[g][g], G1[g + 8][g + 8]
+    const float gsel0 = (g & 1) ? g0[0][1] : g0[0][0];
+    const float gsel1 = (g & 1) ? g1[0][3] : g1[0][2];
+    const float n0 = __shfl_sync(0xffffffffu, gsel0, 4 * g + (g >> 1));
+    const float n1 = __shfl_sync(0xffffffffu, gsel1, 4 * g + (g >> 1));
+    const int64_t w0 = blk * kEmbRows;
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int64_t w = w0 + g + 8 * hr;
+      if (w >= n) continue;
+      const int64_t t = tuple_of(w);
+      const float n2 = hr ? n1 : n0;
+      const float rn = n2 > 0.f ? rsqrtf(n2) : 0.f;  // 1/‖x‖ (≤ 2 ulp); 0 ⇒ cosine 0
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (out[e]) out[e][t] = dd[0][2 * hr + e] * rn * rq[e];
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s) {
   const int64_t n = p.tuple_idx ? p.n_idx : p.n_tuples;
+  if (p.dim % 16 == 0 && p.dim <= 512 && ((uintptr_t)p.item_emb & 15) == 0) {
+    // tensor-core path: 3-stage ring of padded 16-row blocks per warp
+    const int smem = p.use_tmap ? kEmbWarps * kEmbStages * ((p.dim + 63) / 64) * kEmbRows * 128 + 1024
+                                : kEmbWarps * kEmbStages * kEmbRows * (p.dim * 2 + 16);
+    const int64_t n_blk = (n + kEmbRows - 1) / kEmbRows;
+    auto run = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int occ = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEmbWarps * 32, smem);
+      int64_t grid = (int64_t)num_sms() * std::max(occ, 1);
+      grid = std::min<int64_t>(grid, (n_blk + kEmbWarps - 1) / kEmbWarps);
+      kern<<<(unsigned)std::max<int64_t>(grid, 1), kEmbWarps * 32, smem, s>>>(p);
+    };
+    if (p.use_tmap) {
+      if (p.dim <= 128) run(embed_mma_kernel<8, true>);
+      else if (p.dim <= 256) run(embed_mma_kernel<16, true>);
+      else run(embed_mma_kernel<32, true>);
+    } else {
+      if (p.dim <= 128) run(embed_mma_kernel<8, false>);
+      else if (p.dim <= 256) run(embed_mma_kernel<16, false>);
+      else run(embed_mma_kernel<32, false>);
+    }
+    return cudaGetLastError();
+  }
   int64_t blocks = (n + 31) / 32;  // 8 warps × 4 tuples
   blocks = std::min<int64_t>(blocks, (int64_t)num_sms() * 8);
   if (blocks < 1) blocks = 1;
