@@ -575,12 +575,14 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   }();
   int group_of_op[KO_MAX_OPS] = {-1, -1, -1, -1};
   int group_ops[KO_MAX_OPS][KO_MAX_OPS], group_n[KO_MAX_OPS] = {0, 0, 0, 0}, n_groups = 0;
-  auto packs = [&](const int* sel, int n) {
+  // fusing stays within 4 W·V tiles; an operator alone may take up to kMaxTNT (e.g. an 8-class
+  // fp32 map on 16 rows)
+  auto packs = [&](const int* sel, int n, int max_nt) {
     if (n * rows_per_op > KO_MAX_ROWS) return false;
     ko::ScoreParams tsp;
     ko::PrepParams tpp;
     const int nt = pack_table(ops, sel, n, rows_per_op, tsp, tpp);
-    return nt > 0 && nt <= 4;
+    return nt > 0 && nt <= max_nt;
   };
   for (int i = 0; i < P.n_stages; ++i) {
     const int o = P.stage[i].op;
@@ -592,13 +594,13 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
       int sel[KO_MAX_OPS];
       for (int k = 0; k < group_n[c]; ++k) sel[k] = group_ops[c][k];
       sel[group_n[c]] = o;
-      if (packs(sel, group_n[c] + 1)) g = c;
+      if (packs(sel, group_n[c] + 1, 4)) g = c;
     }
     if (g < 0) {
       g = n_groups++;
-      if (!packs(&o, 1))
-        return fail(KO_EUNSUPPORTED, "routed mode: op %d needs more than 4 W·V tiles (%d classes, %s W)",
-                    o, ops[o].n_classes, ops[o].w_is_bf16 ? "bf16" : "fp32");
+      if (!packs(&o, 1, ko::kMaxTNT))
+        return fail(KO_EUNSUPPORTED, "routed mode: op %d needs more than %d W·V tiles (%d classes, %s W)",
+                    o, ko::kMaxTNT, ops[o].n_classes, ops[o].w_is_bf16 ? "bf16" : "fp32");
     }
     group_of_op[o] = g;
     group_ops[g][group_n[g]++] = o;

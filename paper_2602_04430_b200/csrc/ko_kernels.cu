@@ -1617,7 +1617,7 @@ cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1,
   KO_DISPATCH_NOLO(DD, 2, 1) KO_DISPATCH_NOLO(DD, 4, 1) KO_DISPATCH_NOLO(DD, 8, 1)          \
   KO_DISPATCH_TBL(DD, 1, 1) KO_DISPATCH_TBL(DD, 1, 2) KO_DISPATCH_TBL(DD, 1, 4)             \
   KO_DISPATCH_TBL(DD, 2, 1) KO_DISPATCH_TBL(DD, 2, 2) KO_DISPATCH_TBL(DD, 2, 4)             \
-  KO_DISPATCH_TBL(DD, 4, 2) KO_DISPATCH_TBL(DD, 4, 4)                                      \
+  KO_DISPATCH_TBL(DD, 4, 2) KO_DISPATCH_TBL(DD, 4, 4) KO_DISPATCH_TBL(DD, 4, 8)             \
   KO_DISPATCH_TBL(DD, 8, 4) KO_DISPATCH_TBL(DD, 8, 8)
   KO_DISPATCH_D(64)
   KO_DISPATCH_D(128)

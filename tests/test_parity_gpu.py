@@ -316,3 +316,25 @@ def test_routed_subset_and_launch_count(ko):
                          cg[:, :, sub], [plan], wl.spec.op_classes, gold[:, sub])
     # C4's plan: one fused group; positions 0, 1, 3, 5 launched (2 and 4 are covered by 0)
     assert launches == 1 + 2 * 4 + 1
+
+
+def test_routed_wide_map_alone(ko):
+    """A 4-class fp32-readout map on 16 rows per kv-head (G = 4, n_q = 4): 8 W·V entries per row
+    need 8 table tiles, so the operator runs alone in its group; routed margins and counts still
+    match the oracle."""
+    geom = Geom(1, 1, 4, 64, 4)
+    rng = np.random.default_rng(8)
+    lengths = [3, 16, 40, 77, 128]
+    K, V, ops_h = random_problem(rng, geom, lengths, n_ops=1, classes=(4,))
+    pool, indptr, ids, sl = build_pool(K, V, lengths, poison=True)
+    variants = [(300, 1), (1000, 1)]
+    m_or, c_or = oracle.score(geom, pool, indptr, ids, sl, ops_h, variants)
+    th = float(np.quantile(m_or[0, 0], 0.5))
+    plan = [(0, 0, th, th, 0), (0, 1, 0.0, 0.0, 1)]
+    gold = c_or[0, 1][None].astype(np.uint8)
+    kv, ops = tensors_to_device(pool, indptr, ids, sl, geom, ops_h)
+    m, c, counts = ko.score_batch(kv, ops, variants, plans=[plan], gold=torch.from_numpy(gold).cuda())
+    torch.cuda.synchronize()
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    parity.assert_margins(mg, m_or, mask=np.isfinite(mg))
+    parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], [4], gold)
