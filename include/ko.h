@@ -142,11 +142,19 @@ typedef struct {
  *     plan is evaluated per tuple in the same kernel and its counts accumulated.
  *   - n_plans == 1 ("routed mode", P:176-180 cascades): stages execute in order; only tuples
  *     reaching a stage are scored for it (the rest of the margins are left NaN), which is the
- *     runtime saving cascades exist for.
+ *     runtime saving cascades exist for.  Each tuple's cache is read once, up to the
+ *     largest extent its reached stages need: the plan's operators share one read while they fit
+ *     one 16-row tile (an operator's margin may be computed for a tuple that never reaches its
+ *     stage — never written, same bytes), and a later, larger variant resumes from the softmax
+ *     state saved at the end of the earlier extent.  Margins are bitwise
+ *     reproducible; they may differ in the last bits from grid mode's (different summation
+ *     split), within the parity tolerance.
  * gold:      device uint8 [n_ops][n_tuples] (filter 0/1, map class) or NULL: then TP/FP/FN and
  *            n_gold stay 0 (execution on unlabelled data).
  * counts:    device int64 [n_plans][KO_COUNTS_PER_PLAN], accumulated (+=).
- * workspace: device scratch of >= ko_workspace_size(...) bytes, 256-byte aligned.
+ * workspace: device scratch of >= ko_workspace_size(...) bytes, 256-byte aligned (per-tuple
+ *            partial logits and, for routed mode, saved softmax states: O(n_tuples · n_layers ·
+ *            n_kv_heads · n_ops · (n_variants · classes + 8·(4 + 2·tiles))) floats).
  * Errors: KO_EINVAL for NULL required pointers, head_dim not in {64,128}, keep_permille outside
  *   [1,1000], layer_cut outside [1,n_layers], theta_lo > theta_hi, a final filter stage with
  *   theta_lo != theta_hi, a referenced op with no final stage or a stage after its final stage,
