@@ -99,16 +99,30 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
         }
         __syncthreads();
       }
-    // gather: rank r ← token idx[r]; 16-byte chunks of the K and V rows
-    const int chunks = D / 8;
-    for (int w = threadIdx.x; w < L * 2 * chunks; w += blockDim.x) {
-      const int r = w / (2 * chunks), rem = w - r * 2 * chunks;
-      const int which = rem / chunks, ch = rem - which * chunks;
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(src_row(which, idx[r]) + ch * 8));
-      const int64_t page = p.dst_ids[pbase + r / 16];
-      uint16_t* dst = p.dst_pool + (size_t)page * p.page_elems +
-                      ((((size_t)l * 2 + which) * H + h) * 16 + r % 16) * D + ch * 8;
-      *reinterpret_cast<uint4*>(dst) = v;
+    // gather: rank r ← token idx[r]; 16-byte chunks of the K and V rows, 4 loads in flight per
+    // thread before their stores (the copy is latency-bound otherwise)
+    const int chunks = D / 8;  // a power of two (D ∈ {64, 128}): shifts, not divisions
+    const int cs = chunks == 16 ? 4 : 3;
+    const int n_chunk = L * 2 * chunks;
+    constexpr int kU = 4;
+    for (int w0 = threadIdx.x; w0 < n_chunk; w0 += kU * blockDim.x) {
+      uint4 v[kU];
+      uint16_t* dst[kU];
+#pragma unroll
+      for (int k = 0; k < kU; ++k) {
+        const int w = w0 + k * blockDim.x;
+        dst[k] = nullptr;
+        if (w < n_chunk) {
+          const int r = w >> (cs + 1), which = (w >> cs) & 1, ch = w & (chunks - 1);
+          v[k] = __ldg(reinterpret_cast<const uint4*>(src_row(which, idx[r]) + ch * 8));
+          const int64_t page = p.dst_ids[pbase + r / 16];
+          dst[k] = p.dst_pool + (size_t)page * p.page_elems +
+                   ((((size_t)l * 2 + which) * H + h) * 16 + r % 16) * D + ch * 8;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kU; ++k)
+        if (dst[k]) *reinterpret_cast<uint4*>(dst[k]) = v[k];
     }
   }
 }
