@@ -204,11 +204,13 @@ def ncu_traffic(workload_key):
     return None if e is None else e.get("dram_bytes_per_launch")
 
 
-def oracle_sample(wl, seconds, rank_offset=0):
-    """Time the oracle as it stands on a bounded, deterministic sample of the workload."""
+def oracle_sample(wl, seconds, rank_offset=0, threads=None, one_thread=True):
+    """Time the oracle as it stands on a bounded, deterministic sample of the workload (all host
+    cores; plus a 1-thread rate on a quarter of the budget)."""
     import oracle
     import kogen
-    threads = len(os.sched_getaffinity(0))
+    all_threads = len(os.sched_getaffinity(0))
+    threads = threads or all_threads
     ops = oracle.workload_ops(wl)
     done, t_used, batch, start_t = 0, 0.0, 16, rank_offset
     stride = max(1, wl.n_tuples // 997)
@@ -222,10 +224,15 @@ def oracle_sample(wl, seconds, rank_offset=0):
         t_used += time.perf_counter() - t0
         done += batch
         batch = min(256, batch * 2)
-    return dict(value=done / t_used, unit=UNIT, cores=threads, kind="oracle",
-                sample=f"{done} tuples of {wl.name} (every {stride}-th id), all ops x variants "
-                       f"scored + {len(wl.plans)} plans, fp64, input generation excluded",
-                seconds=round(t_used, 2))
+    out = dict(value=done / t_used, unit=UNIT, cores=threads, kind="oracle",
+               sample=f"{done} tuples of {wl.name} (every {stride}-th id), all ops x variants "
+                      f"scored + {len(wl.plans)} plans, fp64, input generation excluded",
+               seconds=round(t_used, 2))
+    if one_thread and threads > 1:
+        o1 = oracle_sample(wl, seconds / 4, rank_offset, threads=1, one_thread=False)
+        out["value_1_thread"] = o1["value"]
+        out["sample_1_thread"] = o1["sample"]
+    return out
 
 
 # ------------------------------------------------------------------------------------------
