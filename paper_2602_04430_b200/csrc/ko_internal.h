@@ -204,6 +204,13 @@ cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s);
 
 // launchers (ko_kernels.cu); return cudaSuccess or the launch error
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
+// per-translation-unit instantiations of the scoring kernel (ko_score_*.cu)
+cudaError_t launch_score_d128_grid(const ScoreParams& p, int CPR0, int CPR1, bool nolo,
+                                   int64_t max_units, cudaStream_t s);
+cudaError_t launch_score_d128_tbl(const ScoreParams& p, int CPR0, int tnt, int64_t max_units,
+                                  cudaStream_t s);
+cudaError_t launch_score_d64(const ScoreParams& p, int CPR0, int CPR1, bool nolo, int tnt,
+                             int64_t max_units, cudaStream_t s);
 // tnt > 0: table-packed kernel with tnt W·V tiles (CPR0 = class stride of the partials)
 cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, bool nolo,
                          int tnt, int64_t max_units, cudaStream_t s);
