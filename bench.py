@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-gb", type=float, default=24.0,
                     help="pinned host memory per rank for the e2e batch")
-    ap.add_argument("--mode", default="pass", choices=["pass", "soft", "embed", "build"],
+    ap.add_argument("--mode", default="pass", choices=["pass", "soft", "embed", "build", "reduce"],
                     help="pass: the hot path (default); soft / embed / build: NEXT-1/3/4 kernels")
     return ap.parse_args()
 
@@ -453,6 +453,30 @@ def run_next(args):
                 "n_stages": S, "params": 3 * S, "tuple_params_per_s": items / (ms / 1000.0),
                 "workspace_gbs": traffic / (ms / 1000.0) / 1e9, "peak_gbs": peak,
                 "config": {"workload": "C5 margins (50k tuples), plan " + str(plan)}}
+    elif args.mode == "reduce":
+        # ko_reduce_stats (the plan-grid reduction on a precomputed ProfileMatrix, §8(b)) and
+        # ko_route (a whole routed plan on precomputed margins) over C5's 50 k × 6 margins
+        wl = workloads.get("C5")
+        n = args.n_tuples or wl.bench_n
+        d = device_workload(wl, n=n, placement="contiguous")
+        m, c, _ = ko.score_batch(d["kv"], d["ops"], wl.variants)
+        counts = torch.zeros((len(wl.plans), ko.COUNTS_PER_PLAN), dtype=torch.int64, device="cuda")
+        ms_r = _time(lambda: ko.reduce_stats(wl.plans, m, c, wl.spec.op_classes, gold=d["gold"],
+                                             counts=counts), args.steps, args.warmup)
+        st = torch.ones(n, dtype=torch.int32, device="cuda")
+        wlist = torch.empty(n, dtype=torch.int32, device="cuda")
+        wlen = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+        def route():
+            st.fill_(1)
+            ko.route(wl.plans[0], m, c, wl.spec.op_classes, -1, st, wlist, wlen, gold=d["gold"])
+        ms_t = _time(route, args.steps, args.warmup)
+        line = {"mode": "reduce", "metric": "plan evaluations on precomputed margins / s",
+                "unit": "tuple-plans/s", "value": n * len(wl.plans) / (ms_r / 1000.0),
+                "ms_per_step": ms_r, "n_tuples": n, "n_plans": len(wl.plans),
+                "route_whole_plan_ms": ms_t,
+                "config": {"workload": f"C5 margins ({n} tuples x {len(wl.variants)} variants x "
+                                       f"{wl.spec.n_ops} ops), {len(wl.plans)}-plan grid"}}
     elif args.mode == "build":
         wl = workloads.get("C2")
         n = args.n_tuples or 2000
