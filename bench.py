@@ -461,8 +461,17 @@ def run_next(args):
         d = device_workload(wl, n=n, placement="contiguous")
         m, c, _ = ko.score_batch(d["kv"], d["ops"], wl.variants)
         counts = torch.zeros((len(wl.plans), ko.COUNTS_PER_PLAN), dtype=torch.int64, device="cuda")
-        ms_r = _time(lambda: ko.reduce_stats(wl.plans, m, c, wl.spec.op_classes, gold=d["gold"],
-                                             counts=counts), args.steps, args.warmup)
+        # captured in a CUDA graph: the per-call ctypes marshalling of 64 plans (≈ 0.1 ms of
+        # Python) would otherwise dominate the device time of this small kernel
+        g = torch.cuda.CUDAGraph()
+        sg = torch.cuda.Stream()
+        sg.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(sg):
+            ko.reduce_stats(wl.plans, m, c, wl.spec.op_classes, gold=d["gold"], counts=counts)
+            with torch.cuda.graph(g, stream=sg):
+                ko.reduce_stats(wl.plans, m, c, wl.spec.op_classes, gold=d["gold"], counts=counts)
+        torch.cuda.current_stream().wait_stream(sg)
+        ms_r = _time(g.replay, args.steps, args.warmup)
         st = torch.ones(n, dtype=torch.int32, device="cuda")
         wlist = torch.empty(n, dtype=torch.int32, device="cuda")
         wlen = torch.zeros(1, dtype=torch.int64, device="cuda")

@@ -338,3 +338,41 @@ def test_routed_wide_map_alone(ko):
     mg, cg = m.cpu().numpy(), c.cpu().numpy()
     parity.assert_margins(mg, m_or, mask=np.isfinite(mg))
     parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], [4], gold)
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_cuda_graph_capture_replay(ko, cfg):
+    """The whole pass (routed C4 / grid C5) is asynchronous on the caller's stream with no host
+    synchronisation, so it can be captured once in a CUDA graph and replayed: replays give the
+    eager call's margins and counts bit for bit."""
+    wl = workloads.get(cfg)
+    n = 2000
+    d = device_workload(wl, n=n)
+    nv, no = len(wl.variants), wl.spec.n_ops
+    m = torch.empty((no, nv, n), dtype=torch.float32, device="cuda")
+    c = torch.empty((no, nv, n), dtype=torch.int32, device="cuda")
+    counts = torch.zeros((len(wl.plans), ko.COUNTS_PER_PLAN), dtype=torch.int64, device="cuda")
+    ws = ko.alloc_workspace(d["kv"], d["ops"], nv, n)
+
+    def step():
+        counts.zero_()
+        ko.score_batch(d["kv"], d["ops"], wl.variants, margins=m, classes=c, plans=wl.plans,
+                       gold=d["gold"], counts=counts, workspace=ws)
+
+    step()
+    torch.cuda.synchronize()
+    m0, c0, k0 = m.clone(), c.clone(), counts.clone()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            step()
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(2):
+        m.fill_(7.0)
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(torch.nan_to_num(m, nan=-9.0), torch.nan_to_num(m0, nan=-9.0))
+    assert torch.equal(c[torch.isfinite(m0)], c0[torch.isfinite(m0)])
+    assert torch.equal(counts, k0)
