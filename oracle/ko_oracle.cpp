@@ -253,9 +253,11 @@ int oracle_run_plans(const or_plan* plans, int32_t n_plans, const double* margin
       if (in_out && in_gold && maps_ok) cnt[0] += 1;
       if (final_alive) final_alive[(size_t)g * n + t] = in_out ? 1 : 0;
     }
-    // FP = |P_o| − TP, FN = |P_g| − TP (accumulated form: recompute from running totals)
-    cnt[1] = cnt[3] - cnt[0];
-    cnt[2] = cnt[4] - cnt[0];
+    // FP = |P_o| − TP, FN = |P_g| − TP (accumulated form: recompute from running totals).
+    // Without labels (gold == NULL) TP/FP/FN/|P_g| are undefined and stay 0 (ko.h contract,
+    // SURVEY §8(b)); only |P_o| and the per-stage counts are produced.
+    cnt[1] = gold ? cnt[3] - cnt[0] : 0;
+    cnt[2] = gold ? cnt[4] - cnt[0] : 0;
   }
   return 0;
 }

@@ -106,14 +106,15 @@ __device__ uint32_t eval_plan(const ko_plan& P, const float* ms, const int32_t* 
 }
 
 // Flush per-CTA int32 counters (FP/FN derived from n_out/n_gold/TP) into the int64 output.
-__device__ void flush_counts(int* s_cnt, int n_rows, unsigned long long* counts) {
+// Without labels (has_gold false) TP/FP/FN/|P_g| stay 0 (ko.h: execution on unlabelled data).
+__device__ void flush_counts(int* s_cnt, int n_rows, unsigned long long* counts, bool has_gold) {
   __syncthreads();
   for (int i = threadIdx.x; i < n_rows * kCountsPerPlan; i += blockDim.x) {
     const int k = i % kCountsPerPlan;
     const int* row = s_cnt + (i - k);
     long long v = s_cnt[i];
-    if (k == KO_C_FP) v = (long long)row[KO_C_OUT] - row[KO_C_TP];
-    if (k == KO_C_FN) v = (long long)row[KO_C_GOLD] - row[KO_C_TP];
+    if (k == KO_C_FP) v = has_gold ? (long long)row[KO_C_OUT] - row[KO_C_TP] : 0;
+    if (k == KO_C_FN) v = has_gold ? (long long)row[KO_C_GOLD] - row[KO_C_TP] : 0;
     if (v) atomicAdd(&counts[i], (unsigned long long)v);
   }
 }

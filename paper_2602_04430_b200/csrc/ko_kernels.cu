@@ -216,7 +216,7 @@ __global__ void route_plan_kernel(const __grid_constant__ RouteParams p) {
     }
     if (p.worklist) append(alive, (int32_t)t, p.worklist, p.worklist_len);
   }
-  flush_counts(s_cnt, 1, p.counts);
+  flush_counts(s_cnt, 1, p.counts, p.gold != nullptr);
 }
 
 // TP/FP/FN/|P_o|/|P_g| from the final tuple states of a routed execution
@@ -251,8 +251,8 @@ __global__ void final_counts_kernel(const __grid_constant__ RouteParams p) {
   __syncthreads();
   for (int k = threadIdx.x; k < 5; k += blockDim.x) {
     long long v = s_cnt[k];
-    if (k == KO_C_FP) v = (long long)s_cnt[KO_C_OUT] - s_cnt[KO_C_TP];
-    if (k == KO_C_FN) v = (long long)s_cnt[KO_C_GOLD] - s_cnt[KO_C_TP];
+    if (k == KO_C_FP) v = p.gold ? (long long)s_cnt[KO_C_OUT] - s_cnt[KO_C_TP] : 0;
+    if (k == KO_C_FN) v = p.gold ? (long long)s_cnt[KO_C_GOLD] - s_cnt[KO_C_TP] : 0;
     if (v) atomicAdd(&p.counts[k], (unsigned long long)v);
   }
 }
@@ -281,7 +281,7 @@ __global__ void reduce_kernel(const __grid_constant__ ReduceParams p) {
                 s_cnt + gp * kCountsPerPlan);
     __syncwarp();
   }
-  flush_counts(s_cnt, p.n_plans, p.counts);
+  flush_counts(s_cnt, p.n_plans, p.counts, p.gold != nullptr);
 }
 
 // Routed round finaliser (after each walk-mode scoring launch): ONE THREAD PER TUPLE of the round

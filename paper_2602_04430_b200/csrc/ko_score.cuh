@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     have_nxt = false;
     cur = nxt;
   }
-  if (n_cnt_rows) flush_counts(s_cnt, n_cnt_rows, p.counts);
+  if (n_cnt_rows) flush_counts(s_cnt, n_cnt_rows, p.counts, p.gold != nullptr);
 }
 
 // ------------------------------------------------------------------------------------------

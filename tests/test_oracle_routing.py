@@ -269,3 +269,18 @@ def test_invalid_plans_rejected():
         oracle.run_plans([[(0, 0, 1.0, -1.0, 0)]], m, np.zeros(m.shape, np.int32), [1])
     with pytest.raises(ValueError):
         oracle.run_plans([[(0, 5, 0.0, 0.0, 1)]], m, np.zeros(m.shape, np.int32), [1])
+
+
+def test_unlabelled_counts_contract():
+    """gold = None (execution on unlabelled data, ko.h / SURVEY §8(b)): TP/FP/FN/|P_g| stay 0;
+    |P_o| and the per-stage counts are those of the labelled evaluation."""
+    rng = np.random.default_rng(3)
+    m = rng.normal(0, 1, size=(2, 2, 500))
+    c = np.zeros((2, 2, 500), np.int32)
+    gold = (rng.random((2, 500)) < 0.5).astype(np.uint8)
+    plan = [[(0, 0, -0.3, 0.3, 0), (0, 1, 0.0, 0.0, 1), (1, 1, 0.0, 0.0, 1)]]
+    lab = oracle.run_plans(plan, m, c, [1, 1], gold)[0]
+    unl = oracle.run_plans(plan, m, c, [1, 1], None)[0]
+    assert unl[0] == unl[1] == unl[2] == unl[4] == 0
+    assert unl[3] == lab[3] and np.array_equal(unl[5:], lab[5:])
+    assert lab[1] == lab[3] - lab[0]

@@ -376,3 +376,19 @@ def test_cuda_graph_capture_replay(ko, cfg):
     assert torch.equal(torch.nan_to_num(m, nan=-9.0), torch.nan_to_num(m0, nan=-9.0))
     assert torch.equal(c[torch.isfinite(m0)], c0[torch.isfinite(m0)])
     assert torch.equal(counts, k0)
+
+
+def test_routed_without_labels(ko):
+    """Execution on unlabelled data (gold = NULL, §8(b)): TP/FP/FN/|P_g| stay 0, |P_o| and every
+    per-stage count equal the labelled run's (labels never steer routing, Q14)."""
+    wl = workloads.get("C4")
+    n = 1500
+    d = device_workload(wl, n=n)
+    plan = wl.plans[0]
+    _, _, k_gold = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan], gold=d["gold"])
+    m, _, k_none = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan], gold=None)
+    torch.cuda.synchronize()
+    kg, kn = k_gold.cpu().numpy()[0], k_none.cpu().numpy()[0]
+    assert kn[0] == kn[1] == kn[2] == kn[4] == 0
+    assert kn[3] == kg[3] and np.array_equal(kn[5:], kg[5:])
+    assert np.isfinite(m.cpu().numpy()).any()
