@@ -677,9 +677,6 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     sp.n_l = n_l;
     sp.n_lh_all = kv->n_layers * kv->n_kv_heads;
     sp.part_cpr = pow2_at_least(maxc);  // the workspace's partial class stride
-    sp.avail_mask = 0;
-    for (int k = 0; k < n_pv; ++k)
-      if (avail[k] <= r) sp.avail_mask |= 1 << k;
     sp.save_state = 0;
     for (int q = 0; q < P.n_stages; ++q)
       if (pos_group[q] == g && pos_round[q] > r) sp.save_state = 1;

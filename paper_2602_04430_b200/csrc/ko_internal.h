@@ -19,7 +19,7 @@ constexpr int kCountsPerPlan = KO_COUNTS_PER_PLAN;
 constexpr int kThreads = 128;  // score kernel CTA size (4 warps, one work unit per warp)
 constexpr int kMaxTNT = 8;     // W·V tiles of the table-packed kernel (2·kMaxTNT slots per lane)
 
-enum Mode : int32_t { MODE_GRID = 0, MODE_STAGE = 1, MODE_WALK = 2 };
+enum Mode : int32_t { MODE_GRID = 0, MODE_WALK = 2 };
 
 // One launch of the scoring kernel.  "Local" op/variant indices are positions in this launch;
 // op_ids / var_ids map them to the caller's indices (margins layout, plans, gold).
@@ -74,9 +74,7 @@ struct ScoreParams {
   int32_t n_plans;
   const uint8_t* gold;  // [n_ops_total][n_tuples] or NULL
   unsigned long long* counts;  // [n_plans][kCountsPerPlan] (int64 bit pattern)
-  // stage mode: apply plan stage `stage_idx` of `plan` (routed execution)
-  int32_t stage_idx;
-  uint32_t* tuple_state;
+  uint32_t* tuple_state;         // walk mode: per-tuple routing state (ko_route's bit layout)
   // walk mode (routed execution): launch = plan position pos = (operator group, variant rank)
   int32_t pos, n_pos, group, round;
   int32_t pos_group[KO_MAX_STAGES], pos_round[KO_MAX_STAGES];
@@ -89,9 +87,8 @@ struct ScoreParams {
   // walk mode, resumable extents: local variants are ALL the plan's KV variants in rank order
   // (local index = rank); this launch streams, per (tuple, layer), the tokens between the
   // extent of the tuple's previous rank for this group and the extent of rank `round`, resuming
-  // the saved softmax state; partials persist per tuple; avail_mask = local variants whose
-  // margins are complete after this round.
-  int32_t avail_mask;
+  // the saved softmax state; partials persist per tuple (ko_walk_kernel finishes a variant's
+  // margin once var_rank says it is complete).
   int32_t save_state;            // a later rank of this group exists: save the state at the end
   float* rstate;                 // [n_tuples][n_layers][Hkv][8][rstate_w] (this group's slice)
   int32_t rstate_w;              // floats per lane group: M[2], den[2], acc[2·NT]
