@@ -285,11 +285,17 @@ def main():
     from kogen import workloads
     from kogen.device import device_workload
 
+    # one rank per GPU; the modulo only matters for the 2-ranks-on-1-GPU test of this path
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1 or os.environ.get("KO_FORCE_DIST") == "1":  # (forced: exercise NCCL at N = 1)
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("KO_DIST_BACKEND", "nccl")   # gloo: the same path on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     wl = workloads.get(args.config)
     n_per = args.n_tuples or wl.bench_n or wl.n_tuples

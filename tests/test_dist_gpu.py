@@ -26,3 +26,26 @@ def test_bench_nccl_path_single_rank():
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 1 and line["value"] > 0
     assert line["counts_plan0"][3] > 0                   # counts survived the all-reduce
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_bench_two_ranks_one_gpu(cfg):
+    """bench.py's N > 1 path end to end with 2 ranks sharing one GPU (gloo carries the count
+    all-reduce and the max over ranks; on the 8-GPU box it is NCCL): byte-balanced shards (C3) or
+    equal shards (C4), the sum of both ranks' tuples in `value`, counts combined."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    env = dict(os.environ, KO_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--config", cfg, "--n-tuples", "300", "--steps", "3", "--warmup", "3",
+           "--no-e2e", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=280, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1                                  # rank 0 alone prints
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["value"] == pytest.approx(2 * 300 * 3 / (line["ms_per_step"] * 3 / 1000.0))
+    assert line["counts_plan0"][3] > 0
