@@ -231,11 +231,7 @@ ko_status make_tmap(CUtensorMap* map, const ko_kv_cache* kv) {
   return KO_OK;
 }
 
-// Fill the kv/op/variant part of ScoreParams and the matching PrepParams for the selected ops
-// (caller indices op_sel[0..n_sel)) and variants.  Row slots: the selected ops are laid out in
-// descending class count, n_q·gqa rows each, slot = half·8 + g; CPR0 / CPR1 (returned) are the
-// power-of-two class counts of the two halves of the 16-row tile (CPR1 = 0: one half used).
-// Table packing (walk mode).  Lane group g owns S rows g (half 0) and g + 8 (half 1); W·V tile tt
+// Table packing (every scoring launch).  Lane group g owns S rows g (half 0) and g + 8 (half 1); W·V tile tt
 // gives it slot (tt, hr) = A row g + 8·hr, which always accumulates with S-row half hr.  So each
 // half of a lane group offers NT slots.  An S row (op, gqa member, query row) of a C-class op needs
 // C entries (2C for fp32 W: bf16 hi and lo).  A row with ≤ NT entries takes one half; a row with
@@ -298,10 +294,14 @@ int pack_table(const ko_operator* ops, const int* order, int n_sel, int rows_per
   return 0;
 }
 
+// Fill the kv/op/variant part of ScoreParams and the matching PrepParams for the selected ops
+// (caller indices op_sel[0..n_sel)) and variants: local ops in descending class count, the table
+// packing of their rows (NT, returned; 0 = does not fit) and the partial class stride CPR
+// (pow2 ≥ the largest class count, returned).
 void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
                  const ko_operator* ops, const int* op_sel, int n_sel, const ko_variant* variants,
                  const int* var_sel, int n_vsel, int32_t n_ops_total, int32_t n_var_total,
-                 const Workspace& ws, int* CPR0, int* CPR1, int* TNT = nullptr) {
+                 const Workspace& ws, int* CPR, int* NT) {
   std::memset(&sp, 0, sizeof(sp));
   std::memset(&pp, 0, sizeof(pp));
   sp.pool = (const uint16_t*)kv->kv_pool;
@@ -339,9 +339,7 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   for (int i = 0; i < n_sel; ++i) order[i] = op_sel[i];
   std::stable_sort(order, order + n_sel,
                    [&](int a, int b) { return ops[a].n_classes > ops[b].n_classes; });
-  int half_cls[2] = {0, 0};
-  for (int r = 0; r < 16; ++r) { sp.slot_op[r] = -1; pp.slot_op[r] = -1; pp.slot_rem[r] = 0; }
-  int slot = 0;
+  int max_cls = 1;
   for (int i = 0; i < n_sel; ++i) {
     const ko_operator& op = ops[order[i]];
     sp.op_ids[i] = order[i];
@@ -351,29 +349,12 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
     pp.w[i] = op.w_is_bf16 ? nullptr : (const float*)op.w;
     pp.w_bf16[i] = op.w_is_bf16 ? (const uint16_t*)op.w : nullptr;
     pp.op_classes[i] = op.n_classes;
-    for (int r = 0; r < sp.rows_per_op; ++r, ++slot) {
-      sp.slot_op[slot] = i;
-      pp.slot_op[slot] = i;
-      pp.slot_rem[slot] = r;
-      half_cls[slot / 8] = std::max(half_cls[slot / 8], (int)op.n_classes);
-    }
+    max_cls = std::max(max_cls, (int)op.n_classes);
   }
-  *CPR0 = pow2_at_least(std::max(half_cls[0], 1));
-  *CPR1 = half_cls[1] ? pow2_at_least(half_cls[1]) : 0;
-  // bf16 readouts of a multi-class tile: two classes per W·V tile (no lo residual)
-  bool all_bf16 = true;
-  for (int i = 0; i < n_sel; ++i) all_bf16 = all_bf16 && ops[op_sel[i]].w_is_bf16;
-  pp.nolo = all_bf16 && *CPR0 >= 2 && *CPR1 <= 1;
-  pp.tbl_nt = 0;
-  if (TNT) {  // table packing replaces the half/class layout above
-    *TNT = pack_table(ops, order, n_sel, sp.rows_per_op, sp, pp);
-    *CPR0 = pow2_at_least(std::max(half_cls[0], half_cls[1]));
-    *CPR1 = 0;
-    pp.nolo = 0;
-    pp.tbl_nt = *TNT;
-    pp.CPR0 = *CPR0;
-    pp.CPR1 = 0;
-  }
+  // table packing: S rows → lane groups, (row, class[, hi/lo]) entries → W·V tile slots
+  *NT = pack_table(ops, order, n_sel, sp.rows_per_op, sp, pp);
+  *CPR = pow2_at_least(max_cls);
+  pp.tbl_nt = *NT;
   sp.qfrag = ws.qfrag;
   sp.wfrag = ws.wfrag;
   sp.part = ws.part;
@@ -412,10 +393,6 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   pp.head_dim = kv->head_dim;
   pp.n_ops = n_sel;
   pp.rows_per_op = sp.rows_per_op;
-  if (!TNT) {
-    pp.CPR0 = *CPR0;
-    pp.CPR1 = *CPR1;
-  }
   pp.qfrag = ws.qfrag;
   pp.wfrag = ws.wfrag;
 }
@@ -490,30 +467,14 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
       if (is_external(variants[i])) ext[n_ext++] = i; else var_sel[n_int++] = i;
     }
     if (n_int == 0) return fail(KO_EINVAL, "no KV variant to score (all variants external)");
-    int CPR0 = 1, CPR1 = 0, TNT = 0;
+    int CPR = 1, NT = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
     fill_common(sp, pp, kv, ops, op_sel, n_ops, variants, var_sel, n_int, n_ops, n_variants,
-                ws, &CPR0, &CPR1);
-    {
-      // the table packing when it needs fewer W·V tiles than the half/class layout (a K-class map
-      // beside filters: 2 tiles instead of 3, W fragments in registers)
-      const int nt_legacy = pp.nolo ? (CPR0 + 1) / 2 + (CPR1 + 1) / 2 : CPR0 + CPR1;
-      ko::ScoreParams tsp;
-      ko::PrepParams tpp;
-      int tc0 = 1, tc1 = 0, tnt = 0;
-      if (nt_legacy >= 2) {
-        fill_common(tsp, tpp, kv, ops, op_sel, n_ops, variants, var_sel, n_int, n_ops, n_variants,
-                    ws, &tc0, &tc1, &tnt);
-        if (tnt > 0 && tnt < nt_legacy) {
-          sp = tsp;
-          pp = tpp;
-          CPR0 = tc0;
-          CPR1 = 0;
-          TNT = tnt;
-        }
-      }
-    }
+                ws, &CPR, &NT);
+    if (NT <= 0)
+      return fail(KO_EUNSUPPORTED, "operators need more than %d W·V tiles per kv-head row tile",
+                  ko::kMaxTNT);
     sp.n_ext = n_ext;
     for (int i = 0; i < n_ext; ++i) sp.ext_ids[i] = ext[i];
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
@@ -535,8 +496,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
     KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, pp.nolo != 0, TNT,
-                             n_work * sp.n_l * kv->n_kv_heads, s));
+    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR, NT, n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end) KO_CUDA(cudaEventRecord(g_trace_end, s));
     return KO_OK;
   }
@@ -665,12 +625,12 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     // tuples queued there (with round 0 extents, never needed by them)
     const int r = std::max(pos_round[pos], 0);
     if (pos > 0 && g == pos_group[0] && r <= std::max(pos_round[0], 0)) continue;
-    int CPR0 = 1, CPR1 = 0, TNT = 0;
+    int CPR = 1, NT = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
     fill_common(sp, pp, kv, ops, group_ops[g], group_n[g], variants, pv, n_pv, n_ops, n_variants,
-                ws, &CPR0, &CPR1, &TNT);
-    if (TNT <= 0) return fail(KO_EUNSUPPORTED, "routed mode: table packing failed");
+                ws, &CPR, &NT);
+    if (NT <= 0) return fail(KO_EUNSUPPORTED, "routed mode: table packing failed");
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
     int n_l = 1;
     for (int k = 0; k <= r && k < n_pv; ++k) n_l = std::max(n_l, (int)variants[pv[k]].layer_cut);
@@ -717,8 +677,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     }
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
     if (g_trace_begin && pos == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR0, CPR1, false, TNT,
-                             n_work * sp.n_l * kv->n_kv_heads, s));
+    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR, NT, n_work * sp.n_l * kv->n_kv_heads, s));
     KO_LAUNCH(ko::launch_walk(sp, s));
     if (g_trace_end && pos == last_launch) KO_CUDA(cudaEventRecord(g_trace_end, s));
   }

@@ -103,14 +103,13 @@ struct ScoreParams {
 
 struct PrepParams {
   int32_t n_l, n_kv_heads, gqa, n_q, n_layers, head_dim;
-  int32_t n_ops, rows_per_op, CPR0, CPR1;
+  int32_t n_ops, rows_per_op;
   int32_t slot_op[16];   // row slot → local op (-1 = padding)
   int32_t slot_rem[16];  // row slot → row within the op (gqa member * n_q + query row)
   const uint16_t* q[kMaxOps];
   const float* w[kMaxOps];          // fp32 readout, or NULL when w_bf16 is given
   const uint16_t* w_bf16[kMaxOps];  // bf16 readout (ko_operator.w_is_bf16)
-  int32_t nolo;                     // all ops bf16: two classes per W·V tile, no lo part
-  // table packing (tbl_nt > 0): W entry of lane group g, slot k = 2·tile + A-row half:
+  // table packing: W entry of lane group g, slot k = 2·tile + A-row half:
   // −1 unused, else (local op) | rem << 3 | class << 8 | lo << 12 (lo: the fp32 residual part)
   int32_t tbl_nt;
   int32_t tbl_w[8][16];
@@ -201,16 +200,12 @@ cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s);
 
 // launchers (ko_kernels.cu); return cudaSuccess or the launch error
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
-// per-translation-unit instantiations of the scoring kernel (ko_score_*.cu)
-cudaError_t launch_score_d128_grid(const ScoreParams& p, int CPR0, int CPR1, bool nolo,
-                                   int64_t max_units, cudaStream_t s);
-cudaError_t launch_score_d128_tbl(const ScoreParams& p, int CPR0, int tnt, int64_t max_units,
-                                  cudaStream_t s);
-cudaError_t launch_score_d64(const ScoreParams& p, int CPR0, int CPR1, bool nolo, int tnt,
-                             int64_t max_units, cudaStream_t s);
-// tnt > 0: table-packed kernel with tnt W·V tiles (CPR0 = class stride of the partials)
-cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, bool nolo,
-                         int tnt, int64_t max_units, cudaStream_t s);
+// per-translation-unit instantiations of the scoring kernel (ko_score_d128.cu, ko_score_d64.cu)
+cudaError_t launch_score_d128(const ScoreParams& p, int CPR, int NT, int64_t max_units, cudaStream_t s);
+cudaError_t launch_score_d64(const ScoreParams& p, int CPR, int NT, int64_t max_units, cudaStream_t s);
+// scoring kernel with NT table-packed W·V tiles; CPR = class stride of the grid-mode partials
+cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR, int NT, int64_t max_units,
+                         cudaStream_t s);
 // routed round finaliser (margins, plan walk, counts, queueing) after a walk-mode launch_score
 cudaError_t launch_walk(const ScoreParams& p, cudaStream_t s);
 cudaError_t launch_route_reach(const RouteParams& p, cudaStream_t s);  // build worklist for stage

@@ -16,8 +16,7 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
     for (int i = threadIdx.x; i < p.n_plans * (int)(sizeof(ko_plan) / 4); i += blockDim.x)
       reinterpret_cast<uint32_t*>(p.gplans)[i] = reinterpret_cast<const uint32_t*>(p.plans)[i];
   const int KS = p.head_dim / 16;
-  const int NT = p.tbl_nt > 0 ? p.tbl_nt
-               : p.nolo ? (p.CPR0 + 1) / 2 + (p.CPR1 + 1) / 2 : p.CPR0 + p.CPR1;
+  const int NT = p.tbl_nt;
   const int Hq = p.n_kv_heads * p.gqa;
   const int n_lh = p.n_l * p.n_kv_heads;
   const int64_t nq_items = (int64_t)n_lh * KS * 32;
@@ -49,7 +48,7 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
           vals[hr][k] = b;
         }
       }
-    } else if (p.tbl_nt > 0) {
+    } else {
       // table packing: A-row half hr of tile tt at lane group g = slot 2·tt + hr of the table
       for (int hr = 0; hr < 2; ++hr) {
         const int ent = p.tbl_w[g][2 * tt + hr];
@@ -69,44 +68,6 @@ __global__ void prep_kernel(const __grid_constant__ PrepParams p) {
           }
           vals[hr][k] = b;
         }
-      }
-    } else {
-      if (!p.nolo) {
-        // fp32 W: tile (half, class) holds bf16 hi in A rows 0-7 and the lo residual in 8-15
-        const int hs = tt < p.CPR0 ? 0 : 1, c = tt < p.CPR0 ? tt : tt - p.CPR0;
-        const int rho = hs * 8 + g;
-        for (int k = 0; k < 4; ++k) {
-          float w = 0.f;
-          if (p.slot_op[rho] >= 0) {
-            const int o = p.slot_op[rho], rem = p.slot_rem[rho];
-            const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
-            if (c < p.op_classes[o]) {
-              const size_t wi = ((((size_t)c * p.n_layers + l) * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k;
-              w = p.w_bf16[o] ? __bfloat162float(__ushort_as_bfloat16(p.w_bf16[o][wi])) : p.w[o][wi];
-            }
-          }
-          const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-          const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
-          vals[0][k] = __bfloat16_as_ushort(hi);  // A rows 0-7: W_hi
-          vals[1][k] = __bfloat16_as_ushort(lo);  // A rows 8-15: W_lo
-        }
-      } else {
-        // bf16 W (exact): tile = (half, class pair); class 2τ' in A rows 0-7, 2τ'+1 in 8-15
-        const int T0 = (p.CPR0 + 1) / 2;
-        const int hs = tt < T0 ? 0 : 1, c0 = 2 * (tt < T0 ? tt : tt - T0);
-        const int rho = hs * 8 + g;
-        for (int hr = 0; hr < 2; ++hr)
-          for (int k = 0; k < 4; ++k) {
-            uint16_t b = 0;
-            const int c = c0 + hr;
-            if (p.slot_op[rho] >= 0) {
-              const int o = p.slot_op[rho], rem = p.slot_rem[rho];
-              const int jj = h * p.gqa + rem / p.n_q, nq = rem % p.n_q;
-              if (c < p.op_classes[o])
-                b = p.w_bf16[o][((((size_t)c * p.n_layers + l) * Hq + jj) * p.n_q + nq) * p.head_dim + d0 + k];
-            }
-            vals[hr][k] = b;
-          }
       }
     }
     uint4 out;
@@ -730,13 +691,11 @@ cudaError_t launch_prep(const PrepParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR0, int CPR1, bool nolo,
-                         int tnt, int64_t max_units, cudaStream_t s) {
-  // the instantiations live in ko_score_d128_grid.cu / ko_score_d128_tbl.cu / ko_score_d64.cu
-  if (head_dim == 128)
-    return tnt == 0 ? launch_score_d128_grid(p, CPR0, CPR1, nolo, max_units, s)
-                    : launch_score_d128_tbl(p, CPR0, tnt, max_units, s);
-  if (head_dim == 64) return launch_score_d64(p, CPR0, CPR1, nolo, tnt, max_units, s);
+cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR, int NT, int64_t max_units,
+                         cudaStream_t s) {
+  // the instantiations live in ko_score_d128.cu / ko_score_d64.cu
+  if (head_dim == 128) return launch_score_d128(p, CPR, NT, max_units, s);
+  if (head_dim == 64) return launch_score_d64(p, CPR, NT, max_units, s);
   return cudaErrorInvalidValue;
 }
 

@@ -1,4 +1,4 @@
-// ko_score.cuh — the hot kernel ko_score_kernel<D, CPR0, CPR1, NOLO, TNT> and its launcher
+// ko_score.cuh — the hot kernel ko_score_kernel<D, CPR, NT> and its launcher
 // template; instantiated per head_dim and packing family in ko_score_*.cu so the instantiations
 // compile in parallel.
 //
@@ -101,27 +101,16 @@ __device__ __forceinline__ void finalise_tuple(const ScoreParams& p, int64_t wsl
     }
 }
 
-// CPR0 / CPR1: classes per row slot in half 0 (A rows g) / half 1 (A rows g+8) of the row tile;
-// CPR1 = 0 when at most 8 rows attend a kv-head; partial logits are stored with stride
-// CPR = CPR0 (≥ every op's classes).  W·V tiles:
-//   fp32 W (NOLO = false): bf16 hi in A rows 0-7 + lo in rows 8-15 of one tile per (half, class):
-//     tile(h, c) = h ? CPR0 + c : c, u = C[e] + C[2+e];
-//   bf16 W (NOLO = true, exact: no lo part): two classes per tile, class c in rows 0-7 (c even)
-//     or 8-15 (c odd): tile(h, c) = (h ? ⌈CPR0/2⌉ : 0) + c/2, u = C[2(c&1) + e].
-// TNT > 0 (table packing, every walk-mode launch): the W·V tiles are packed per lane group g
-// from a host table — A-row half hr of tile tt at lane group g is slot k = 2·tt + hr, which
-// accumulates with S row g + 8·hr for the (op, class) tgt[k]; a row with more entries than one
-// half's TNT slots is duplicated into both halves.
-template <int D, int CPR0, int CPR1, bool NOLO, int TNT>
+// Table packing: the W·V tiles are packed per lane group g from a host table — A-row half hr of
+// tile tt at lane group g is slot k = 2·tt + hr, which accumulates with S row g + 8·hr for the
+// (op, class) tgt[k]; a row with more entries than one half's NT slots is duplicated into both
+// halves.  CPR: class stride of the grid-mode partials (pow2 ≥ every op's
+// classes); NT: W·V tiles.
+template <int D, int CPR, int NT>
 __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_constant__ ScoreParams p) {
-  constexpr bool TBL = TNT > 0;
   constexpr int KS = D / 16;  // mma k-steps over head_dim
   constexpr int KP = D / 32;  // 128-bit fragment reads per token row per lane (2 k-steps each)
-  constexpr int NH = TBL ? 2 : (CPR1 > 0 ? 2 : 1);
-  constexpr int CPR = CPR0;
-  constexpr int T0 = NOLO ? (CPR0 + 1) / 2 : CPR0;  // tiles of half 0
-  constexpr int NT = TBL ? TNT : (NOLO ? T0 + (CPR1 + 1) / 2 : CPR0 + CPR1);
-  constexpr int NSL = TBL ? 2 * TNT : 1;            // table slots per lane
+  constexpr int NSL = 2 * NT;                       // table slots per lane
   constexpr int WREG = NT <= 2 ? NT : 0;            // W·V tiles whose fragments stay in registers
   constexpr int S = Ring<D>::kStages;
   constexpr int STAGE = Ring<D>::kStageBytes;
@@ -162,10 +151,6 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   // variants whose extents this launch streams: grid = all; walk = ranks ≤ round
   const int v_hi = walk ? p.round : p.n_var - 1;
 
-  // row slot → local op for this lane's two half-slots (legacy packing)
-  int slot_op[NH];
-#pragma unroll
-  for (int hs = 0; hs < NH; ++hs) slot_op[hs] = p.slot_op[hs * 8 + g];
   // table packing: this lane group's slot k = 2·tile + hr (S-row half hr) → target op·8 + class
   int tgt[NSL];
 #pragma unroll
@@ -176,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   uint64_t red0 = 0, red1 = 0;
   uint32_t red_off = 0;
   int red_n = 0;
-  if constexpr (TBL) {
+  {
 #pragma unroll
     for (int k = 0; k < NSL; ++k) tgt[k] = p.tbl_tgt[g][k];
     for (int gg = 0; gg < 8; ++gg)
@@ -353,26 +338,21 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
                       : nullptr;
 
     // lane-local online-softmax state per half-slot (log2 domain)
-    float mx[NH], sm[NH], ac[TBL ? 1 : NH][CPR], at[NSL];
+    float mx[2], sm[2], at[NSL];
 #pragma unroll
-    for (int hs = 0; hs < NH; ++hs) {
-      mx[hs] = TBL ? kNoMax : -CUDART_INF_F;
+    for (int hs = 0; hs < 2; ++hs) {
+      mx[hs] = kNoMax;
       sm[hs] = 0.f;
-#pragma unroll
-      for (int c = 0; c < CPR; ++c)
-        if (!TBL) ac[TBL ? 0 : hs][c] = 0.f;
     }
 #pragma unroll
     for (int k = 0; k < NSL; ++k) at[k] = 0.f;
-    if constexpr (TBL) {
-      if (walk && s0 > 0 && q == 0) {  // resume: the quad's merged state enters through lane q = 0
-        mx[0] = __ldcg(rst + 0);
-        mx[1] = __ldcg(rst + 1);
-        sm[0] = __ldcg(rst + 2);
-        sm[1] = __ldcg(rst + 3);
+    if (walk && s0 > 0 && q == 0) {  // resume: the quad's merged state enters through lane q = 0
+      mx[0] = __ldcg(rst + 0);
+      mx[1] = __ldcg(rst + 1);
+      sm[0] = __ldcg(rst + 2);
+      sm[1] = __ldcg(rst + 3);
 #pragma unroll
-        for (int k = 0; k < NSL; ++k) at[k] = __ldcg(rst + 4 + k);
-      }
+      for (int k = 0; k < NSL; ++k) at[k] = __ldcg(rst + 4 + k);
     }
 
     int snap_lo = s0;  // first token not yet folded into the running state
@@ -447,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       for (;;) {
         const int seg_hi = min(next_snap, page_hi);
         // fold tokens [snap_lo, seg_hi) of this page into the lane-local state
-        if constexpr (TBL) {
+        {
           // running max starts at a finite sentinel (kNoMax): corr and p need no −∞ guards
           float corr[2], ps[2][4];
           const bool full = pg * 16 >= snap_lo && pg * 16 + 16 <= seg_hi;  // warp-uniform
@@ -482,47 +462,11 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
               a = fmaf(ps[hr][kk], U[k >> 1][kk >> 1][2 * hr + (kk & 1)], a);
             at[k] = a;
           }
-        } else {
-#pragma unroll
-        for (int hs = 0; hs < NH; ++hs) {
-          float x[4];
-          float xm = -CUDART_INF_F;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int nt = k >> 1, e = k & 1;
-            const int tok = pg * 16 + nt * 8 + 2 * q + e;
-            const bool in = tok >= snap_lo && tok < seg_hi;
-            x[k] = in ? Sacc[nt][2 * hs + e] * p.scale_log2 : -CUDART_INF_F;
-            xm = fmaxf(xm, x[k]);
-          }
-          const float mn = fmaxf(mx[hs], xm);
-          if (mn != -CUDART_INF_F) {
-            const float corr = ex2(mx[hs] - mn);
-            float ps[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) ps[k] = ex2(x[k] - mn);
-            sm[hs] = sm[hs] * corr + ((ps[0] + ps[1]) + (ps[2] + ps[3]));
-#pragma unroll
-            for (int c = 0; c < (hs == 0 ? CPR0 : CPR1); ++c) {
-              const int tt = NOLO ? (hs == 0 ? 0 : T0) + c / 2 : (hs == 0 ? c : CPR0 + c);
-              float a = ac[TBL ? 0 : hs][c] * corr;
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int nt = k >> 1, e = k & 1;
-                const float u = NOLO ? U[tt][nt][2 * (c & 1) + e] : U[tt][nt][e] + U[tt][nt][2 + e];
-                a = fmaf(ps[k], u, a);
-              }
-              ac[TBL ? 0 : hs][c] = a;
-            }
-            mx[hs] = mn;
-          }
-        }
         }
         snap_lo = seg_hi;
         if (seg_hi == next_snap) {
           // ---- snapshot: merge the quad's lane states, reduce rows per op, emit partials
-          float opv[kMaxOps][CPR];  // legacy packing: per-(op, class) partial (all lanes)
-          if constexpr (TBL) {
+          {
             float Mq[2], f[2], den[2], rden[2];
 #pragma unroll
             for (int hs = 0; hs < 2; ++hs) {
@@ -585,54 +529,6 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
                   p.part[at] = x;
                 }
             }
-          } else {
-          float val[NH][CPR];
-#pragma unroll
-          for (int hs = 0; hs < NH; ++hs) {
-            float M = mx[hs];
-            M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
-            M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
-            const float f = mx[hs] == -CUDART_INF_F ? 0.f : ex2(mx[hs] - M);
-            float den = sm[hs] * f;
-            den += __shfl_xor_sync(0xffffffffu, den, 1);
-            den += __shfl_xor_sync(0xffffffffu, den, 2);
-#pragma unroll
-            for (int c = 0; c < CPR; ++c) {
-              if (c >= (hs == 0 ? CPR0 : CPR1)) { val[hs][c] = 0.f; continue; }
-              float a = ac[TBL ? 0 : hs][c] * f;
-              a += __shfl_xor_sync(0xffffffffu, a, 1);
-              a += __shfl_xor_sync(0xffffffffu, a, 2);
-              val[hs][c] = __fdiv_rn(a, den);
-            }
-          }
-#pragma unroll
-          for (int o = 0; o < kMaxOps; ++o) {
-#pragma unroll
-            for (int c = 0; c < CPR; ++c) {
-              float x = 0.f;
-#pragma unroll
-              for (int hs = 0; hs < NH; ++hs) x += slot_op[hs] == o ? val[hs][c] : 0.f;
-              if (o < p.n_ops) {
-                x += __shfl_xor_sync(0xffffffffu, x, 4);
-                x += __shfl_xor_sync(0xffffffffu, x, 8);
-                x += __shfl_xor_sync(0xffffffffu, x, 16);
-              }
-              opv[o][c] = x;
-            }
-          }
-          }
-          if (!TBL && lane == 0) {  // grid: partials per work slot, local (op, variant) indices
-#pragma unroll
-            for (int v = 0; v < kMaxVar; ++v) {
-              if (nkv[v] != next_snap) continue;
-#pragma unroll
-              for (int o = 0; o < kMaxOps; ++o) {
-                if (o >= p.n_ops) break;
-                float* dst = p.part + ((((size_t)wslot * p.n_l * Hkv + unit_lh) * p.n_ops + o) * p.n_var + v) * CPR;
-#pragma unroll
-                for (int c = 0; c < CPR; ++c) dst[c] = opv[o][c];
-              }
-            }
           }
           next_snap = next_point(next_snap);  // the next larger snapshot point
         }
@@ -680,11 +576,11 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 //   d0 = 64(j/2) + 16q + 8(j%2) + 4e — exactly the 8 consecutive bf16 of the 16-byte chunk
 //   (2q + j%2) of 64-wide box j/2 that lane (g, q) reads from the swizzled TMA stage.
 
-template <int D, int CPR0, int CPR1, bool NOLO, int TNT>
+template <int D, int CPR, int NT>
 cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t s) {
   static int occ = 0;
   constexpr int smem = Ring<D>::kSmemBytes;
-  auto* kern = ko_score_kernel<D, CPR0, CPR1, NOLO, TNT>;
+  auto* kern = ko_score_kernel<D, CPR, NT>;
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);

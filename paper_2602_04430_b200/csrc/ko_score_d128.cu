@@ -1,12 +1,12 @@
-// ko_score_d64.cu — head_dim 64 instantiations of the scoring kernel.
+// ko_score_d128.cu — head_dim 128 instantiations of the scoring kernel.
 #include "ko_score.cuh"
 
 namespace ko {
 
-cudaError_t launch_score_d64(const ScoreParams& p, int CPR, int NT, int64_t max_units,
+cudaError_t launch_score_d128(const ScoreParams& p, int CPR, int NT, int64_t max_units,
                              cudaStream_t s) {
 #define KO_DISPATCH(C, T) \
-  if (CPR == C && NT == T) return launch_score_t<64, C, T>(p, max_units, s);
+  if (CPR == C && NT == T) return launch_score_t<128, C, T>(p, max_units, s);
   // (class stride, tiles) pairs the table packing can produce: a C-class row has C (bf16) or 2C
   // (fp32) entries, at most 2·NT of them per lane group
   KO_DISPATCH(1, 1) KO_DISPATCH(1, 2) KO_DISPATCH(1, 4) KO_DISPATCH(2, 1) KO_DISPATCH(2, 2)
