@@ -94,7 +94,7 @@ struct ScoreParams {
   int32_t rstate_w;              // floats per lane group: M[2], den[2], acc[2·NT]
   int32_t n_lh_all;              // n_layers · Hkv (partials of walk mode are per tuple, all layers)
   int32_t part_cpr;              // class stride of walk-mode partials (same for every group)
-  // table-driven row/class packing (template TNT > 0): per lane group g, W·V slot k = 2·tile + hr
+  // table-driven row/class packing (template NT): per lane group g, W·V slot k = 2·tile + hr
   // (A-row half hr) accumulates with S row g + 8·hr into the local (op, class) target
   // tgt = op·8 + class (−1: unused)
   int8_t tbl_tgt[8][16];
