@@ -392,3 +392,26 @@ def test_routed_without_labels(ko):
     assert kn[0] == kn[1] == kn[2] == kn[4] == 0
     assert kn[3] == kg[3] and np.array_equal(kn[5:], kg[5:])
     assert np.isfinite(m.cpu().numpy()).any()
+
+
+def test_routed_resume_long_sequences(ko):
+    """Routed resume on C3's long variable-length caches (256–4096 tokens, up to 256 pages per
+    kv-head): round 1 restarts past page 32 (a later page-id chunk) from the saved state; reached
+    margins and counts match the oracle."""
+    wl = workloads.get("C3")
+    n = 160
+    d = device_workload(wl, n=n)
+    m_or, c_or = oracle.score_workload(wl, np.arange(n))
+    # C3's variants: (1000,1) (500,1) (200,1) (1000,2) (500,2) (200,2); cascade 200‰/1 → 500‰/2 → gold
+    v_small, v_mid, v_gold = 2, 4, 3
+    q = lambda v, a: float(np.quantile(m_or[0, v], a))
+    plan = [(0, v_small, q(v_small, 0.3), q(v_small, 0.7), 0), (0, v_mid, q(v_mid, 0.4), q(v_mid, 0.6), 0),
+            (0, v_gold, 0.0, 0.0, 1)]
+    m, c, counts = ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan], gold=d["gold"])
+    torch.cuda.synchronize()
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    reached = np.isfinite(mg)
+    assert reached[0, v_gold].any() and not reached[0, v_gold].all()
+    parity.assert_margins(mg, m_or, mask=reached)
+    parity.assert_counts(counts.cpu().numpy(), m_or, c_or, mg, cg, [plan], wl.spec.op_classes,
+                         d["gold"].cpu().numpy())
