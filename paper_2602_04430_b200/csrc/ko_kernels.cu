@@ -219,27 +219,48 @@ __global__ void final_counts_kernel(const __grid_constant__ RouteParams p) {
 }
 
 // G-plan grid on precomputed margins: one warp per tuple, one lane per plan
-__global__ void reduce_kernel(const __grid_constant__ ReduceParams p) {
+// ko_reduce_stats: warp per tuple, lane per plan.  Latency-bound per warp (margin loads, then the
+// plan walks), so CTAs are 32 warps wide: many tuples in flight per SM, while the per-CTA count
+// flush (one global atomic per counter) stays at 2 CTAs per SM.
+constexpr int kReduceThreads = 512;
+__global__ void __launch_bounds__(kReduceThreads, 2) reduce_kernel(const __grid_constant__ ReduceParams p) {
   __shared__ int s_cnt[kMaxPlans * kCountsPerPlan];
   __shared__ ko_plan s_plans[kMaxPlans];  // lanes read different plans: smem, not the param bank
   for (int i = threadIdx.x; i < p.n_plans * (int)(sizeof(ko_plan) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(s_plans)[i] = reinterpret_cast<const uint32_t*>(p.plans)[i];
-  __shared__ float s_m[8][kMaxOps * kMaxVar];
-  __shared__ int32_t s_c[8][kMaxOps * kMaxVar];
+  __shared__ float s_m[kReduceThreads / 32][kMaxOps * kMaxVar];
+  __shared__ int32_t s_c[kReduceThreads / 32][kMaxOps * kMaxVar];
   for (int i = threadIdx.x; i < p.n_plans * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
+  __shared__ uint8_t s_g[kReduceThreads / 32][kMaxOps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  const int nmv = p.n_ops * p.n_variants;
-  for (int64_t t = (int64_t)blockIdx.x * nw + w; t < p.n_tuples; t += (int64_t)gridDim.x * nw) {
-    for (int idx = lane; idx < nmv; idx += 32) {
-      s_m[w][idx] = p.margins[(size_t)idx * p.n_tuples + t];
-      s_c[w][idx] = p.classes ? p.classes[(size_t)idx * p.n_tuples + t] : 0;
+  const int nmv = p.n_ops * p.n_variants;  // ≤ 32: one (op, variant) entry per lane
+  const int64_t stride = (int64_t)gridDim.x * nw;
+  // the next tuple's margins / classes / gold bytes are loaded while this one's plans run
+  auto fetch = [&](int64_t t, float& m, int32_t& c, uint8_t& gv) {
+    m = 0.f; c = 0; gv = 0;
+    if (t >= p.n_tuples) return;
+    if (lane < nmv) {
+      m = p.margins[(size_t)lane * p.n_tuples + t];
+      c = p.classes ? p.classes[(size_t)lane * p.n_tuples + t] : 0;
     }
+    if (p.gold && lane < p.n_ops) gv = p.gold[(size_t)lane * p.n_tuples + t];
+  };
+  float nm;
+  int32_t nc;
+  uint8_t ng;
+  int64_t t = (int64_t)blockIdx.x * nw + w;
+  fetch(t, nm, nc, ng);
+  for (; t < p.n_tuples; t += stride) {
+    if (lane < nmv) { s_m[w][lane] = nm; s_c[w][lane] = nc; }
+    if (lane < kMaxOps) s_g[w][lane] = ng;
     __syncwarp();
+    fetch(t + stride, nm, nc, ng);
+    // gold bytes from shared memory: [op][1] with n_tuples = 1, tuple 0
     for (int gp = lane; gp < p.n_plans; gp += 32)
-      eval_plan(s_plans[gp], s_m[w], s_c[w], p.n_variants, p.n_classes, p.gold, p.n_tuples, t,
-                s_cnt + gp * kCountsPerPlan);
+      eval_plan(s_plans[gp], s_m[w], s_c[w], p.n_variants, p.n_classes,
+                p.gold ? s_g[w] : nullptr, 1, 0, s_cnt + gp * kCountsPerPlan);
     __syncwarp();
   }
   flush_counts(s_cnt, p.n_plans, p.counts, p.gold != nullptr);
@@ -726,7 +747,7 @@ cudaError_t launch_final_counts(const RouteParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 cudaError_t launch_reduce(const ReduceParams& p, cudaStream_t s) {
-  reduce_kernel<<<num_sms() * 2, 256, 0, s>>>(p);
+  reduce_kernel<<<num_sms() * 2, kReduceThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
