@@ -99,30 +99,34 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
         }
         __syncthreads();
       }
-    // gather: rank r ← token idx[r]; 16-byte chunks of the K and V rows, 4 loads in flight per
-    // thread before their stores (the copy is latency-bound otherwise)
+    // gather: rank r ← token idx[r].  The sort keys are dead now, so their 32 KB stage the copy:
+    // per pass every thread issues its 16-byte chunks of the next block of ranks as cp.async
+    // (global → shared, nothing held in registers, all in flight at once), then writes them to
+    // the destination pages.
     const int chunks = D / 8;  // a power of two (D ∈ {64, 128}): shifts, not divisions
     const int cs = chunks == 16 ? 4 : 3;
-    const int n_chunk = L * 2 * chunks;
-    constexpr int kU = 4;
-    for (int w0 = threadIdx.x; w0 < n_chunk; w0 += kU * blockDim.x) {
-      uint4 v[kU];
-      uint16_t* dst[kU];
-#pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        const int w = w0 + k * blockDim.x;
-        dst[k] = nullptr;
-        if (w < n_chunk) {
-          const int r = w >> (cs + 1), which = (w >> cs) & 1, ch = w & (chunks - 1);
-          v[k] = __ldg(reinterpret_cast<const uint4*>(src_row(which, idx[r]) + ch * 8));
-          const int64_t page = p.dst_ids[pbase + r / 16];
-          dst[k] = p.dst_pool + (size_t)page * p.page_elems +
-                   ((((size_t)l * 2 + which) * H + h) * 16 + r % 16) * D + ch * 8;
-        }
+    const int per_rank = 2 * chunks;                         // K and V row chunks of one rank
+    const int ranks_pass = (kBuildMaxTokens * (int)sizeof(double)) / (per_rank * 16);
+    const uint32_t stage = (uint32_t)__cvta_generic_to_shared(key);
+    __syncthreads();  // every thread is done with key[] (the sort's last phase)
+    for (int r0 = 0; r0 < L; r0 += ranks_pass) {
+      const int n_c = min(ranks_pass, L - r0) * per_rank;
+      for (int w = threadIdx.x; w < n_c; w += blockDim.x) {
+        const int r = r0 + (w >> (cs + 1)), which = (w >> cs) & 1, ch = w & (chunks - 1);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage + 16u * (uint32_t)w),
+                     "l"(src_row(which, idx[r]) + ch * 8)
+                     : "memory");
       }
-#pragma unroll
-      for (int k = 0; k < kU; ++k)
-        if (dst[k]) *reinterpret_cast<uint4*>(dst[k]) = v[k];
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+      __syncthreads();
+      for (int w = threadIdx.x; w < n_c; w += blockDim.x) {
+        const int r = r0 + (w >> (cs + 1)), which = (w >> cs) & 1, ch = w & (chunks - 1);
+        const int64_t page = p.dst_ids[pbase + r / 16];
+        uint16_t* dst = p.dst_pool + (size_t)page * p.page_elems +
+                        ((((size_t)l * 2 + which) * H + h) * 16 + r % 16) * D + ch * 8;
+        *reinterpret_cast<uint4*>(dst) = reinterpret_cast<const uint4*>(key)[w];
+      }
+      __syncthreads();  // the stage is reused by the next pass
     }
   }
 }
