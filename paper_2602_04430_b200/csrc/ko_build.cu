@@ -36,8 +36,8 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
   extern __shared__ __align__(16) unsigned char smem[];
   double* key = reinterpret_cast<double*>(smem);                  // [N]
   int* idx = reinterpret_cast<int*>(key + kBuildMaxTokens);       // [N]
-  float* s_mu = reinterpret_cast<float*>(idx + kBuildMaxTokens);  // [D]
-  float* s_s2 = s_mu + p.head_dim;                                // [D]
+  double* s_mu = reinterpret_cast<double*>(idx + kBuildMaxTokens);  // [D] (exact fp32 → fp64)
+  double* s_s2 = s_mu + p.head_dim;                                 // [D]
   const int D = p.head_dim, H = p.n_kv_heads, Lyr = p.n_layers;
   const int64_t n_units = p.n_tuples * Lyr * H;
   for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -47,15 +47,16 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
     if (L < 1 || L > kBuildMaxTokens) continue;  // documented limit (device data: skipped)
     __syncthreads();
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
-      s_mu[d] = p.mu[((size_t)l * H + h) * D + d];
-      s_s2[d] = p.sigma2[((size_t)l * H + h) * D + d];
+      s_mu[d] = (double)p.mu[((size_t)l * H + h) * D + d];
+      s_s2[d] = (double)p.sigma2[((size_t)l * H + h) * D + d];
     }
     __syncthreads();
     const int64_t pbase = p.indptr[t];
+    // element offset of (layer l, K/V, kv-head h, slot 0) inside a page; slot s adds s·D
+    const int off_k = ((l * 2 + 0) * H + h) * 16 * D, off_v = ((l * 2 + 1) * H + h) * 16 * D;
     auto src_row = [&](int which, int i) -> const uint16_t* {
-      const int64_t page = p.src_ids[pbase + i / 16];
-      return p.src_pool + (size_t)page * p.page_elems +
-             ((((size_t)l * 2 + which) * H + h) * 16 + i % 16) * D;
+      const int64_t page = p.src_ids[pbase + (i >> 4)];
+      return p.src_pool + (size_t)page * p.page_elems + (which ? off_v : off_k) + (i & 15) * D;
     };
     int N = 1;
     while (N < L) N <<= 1;
@@ -69,8 +70,8 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const double x = bf16_to_double((uint16_t)(e & 1 ? w[e >> 1] >> 16 : w[e >> 1] & 0xFFFFu));
-            a = __dadd_rn(a, __dmul_rn((double)s_mu[d + e], x));
-            b = __dadd_rn(b, __dmul_rn((double)s_s2[d + e], __dmul_rn(x, x)));
+            a = __dadd_rn(a, __dmul_rn(s_mu[d + e], x));
+            b = __dadd_rn(b, __dmul_rn(s_s2[d + e], __dmul_rn(x, x)));
           }
         }
         key[i] = __dadd_rn(__dmul_rn(a, p.inv_sqrt_d), __dmul_rn(b, p.inv_2d));
@@ -121,9 +122,9 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
       __syncthreads();
       for (int w = threadIdx.x; w < n_c; w += blockDim.x) {
         const int r = r0 + (w >> (cs + 1)), which = (w >> cs) & 1, ch = w & (chunks - 1);
-        const int64_t page = p.dst_ids[pbase + r / 16];
-        uint16_t* dst = p.dst_pool + (size_t)page * p.page_elems +
-                        ((((size_t)l * 2 + which) * H + h) * 16 + r % 16) * D + ch * 8;
+        const int64_t page = p.dst_ids[pbase + (r >> 4)];
+        uint16_t* dst = p.dst_pool + (size_t)page * p.page_elems + (which ? off_v : off_k) +
+                        (r & 15) * D + ch * 8;
         *reinterpret_cast<uint4*>(dst) = reinterpret_cast<const uint4*>(key)[w];
       }
       __syncthreads();  // the stage is reused by the next pass
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
 }  // namespace
 
 size_t build_smem_bytes(int head_dim) {
-  return (size_t)kBuildMaxTokens * (sizeof(double) + sizeof(int)) + 2 * sizeof(float) * head_dim;
+  return (size_t)kBuildMaxTokens * (sizeof(double) + sizeof(int)) + 2 * sizeof(double) * head_dim;
 }
 
 cudaError_t launch_build(const BuildParams& p, cudaStream_t s) {
