@@ -615,16 +615,23 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   // A position whose (group, round) is covered by position 0 never receives a tuple (position 0
   // processes every tuple), so it is not launched.
   KO_CUDA(cudaMemsetAsync(ws.round_len, 0, sizeof(unsigned long long) * KO_MAX_STAGES, s));
+  // Launched positions.  A stage on an external variant (e.g. the embedding pre-filter) streams
+  // nothing: position 0 on one only walks every tuple (deciding it from the caller's margins and
+  // queueing the survivors), and a later one never receives a tuple (its margin is always
+  // available).  A KV position whose (group, round) position 0 already streamed is covered.
+  auto launched = [&](int pos) {
+    if (pos == 0) return true;
+    if (pos_round[pos] < 0) return false;
+    return !(pos_round[0] >= 0 && pos_group[pos] == pos_group[0] && pos_round[pos] <= pos_round[0]);
+  };
   int last_launch = 0, prepped_group = -1;
   for (int pos = 0; pos < P.n_stages; ++pos)
-    if (pos == 0 || !(pos_group[pos] == pos_group[0] && std::max(pos_round[pos], 0) <= std::max(pos_round[0], 0)))
-      last_launch = pos;
+    if (launched(pos)) last_launch = pos;
   for (int pos = 0; pos < P.n_stages; ++pos) {
+    if (!launched(pos)) continue;
     const int g = pos_group[pos];
-    // a stage on an external variant computes nothing itself; its launch still walks the
-    // tuples queued there (with round 0 extents, never needed by them)
+    const bool walk_only = pos_round[pos] < 0;  // external stage at position 0
     const int r = std::max(pos_round[pos], 0);
-    if (pos > 0 && g == pos_group[0] && r <= std::max(pos_round[0], 0)) continue;
     int CPR = 1, NT = 0;
     ko::ScoreParams sp;
     ko::PrepParams pp;
@@ -644,7 +651,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     sp.rstate_w = ws.rstate_w;
     sp.pos = pos;
     sp.n_pos = P.n_stages;
-    sp.group = g;
+    sp.group = walk_only ? -1 : g;  // −1: the walk records no computed round
     sp.round = r;
     for (int q = 0; q < P.n_stages; ++q) {
       sp.pos_group[q] = pos_group[q];
@@ -671,13 +678,15 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     sp.tuple_state = ws.tuple_state;
     sp.tuple_done = ws.tuple_done;
     sp.counts = (unsigned long long*)counts;
-    if (g != prepped_group) {  // the fragments depend only on the group (all plan layers)
-      KO_LAUNCH(ko::launch_prep(pp, s));
-      prepped_group = g;
-    }
-    KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
     if (g_trace_begin && pos == 0) KO_CUDA(cudaEventRecord(g_trace_begin, s));
-    KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR, NT, n_work * sp.n_l * kv->n_kv_heads, s));
+    if (!walk_only) {
+      if (g != prepped_group) {  // the fragments depend only on the group (all plan layers)
+        KO_LAUNCH(ko::launch_prep(pp, s));
+        prepped_group = g;
+      }
+      KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 8, s));
+      KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR, NT, n_work * sp.n_l * kv->n_kv_heads, s));
+    }
     KO_LAUNCH(ko::launch_walk(sp, s));
     if (g_trace_end && pos == last_launch) KO_CUDA(cudaEventRecord(g_trace_end, s));
   }

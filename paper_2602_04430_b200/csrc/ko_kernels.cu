@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kWalkThreads) ko_walk_kernel(const __grid_cons
       t = p.work ? (int64_t)p.work[w] : w;
       uint32_t state = p.pos == 0 ? 1u : __ldcg(p.tuple_state + t);
       uint32_t done = p.pos == 0 ? 0xFFFFFFFFu : __ldcg(p.tuple_done + t);  // 4-bit round+1 per group
-      {
+      if (p.group >= 0) {  // −1: a walk-only launch (external stage at position 0) computed nothing
         const uint32_t cur = (done >> (4 * p.group)) & 15u;
         const uint32_t mine = (uint32_t)p.round + 1u;
         if (cur == 15u || cur < mine) done = (done & ~(15u << (4 * p.group))) | (mine << (4 * p.group));

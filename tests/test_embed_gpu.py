@@ -62,6 +62,10 @@ def test_embedding_first_stage_cascade(ko):
     m, c, counts = ko.score_batch(d["kv"], d["ops"], variants, margins=margins, plans=[plan],
                                   gold=d["gold"])
     torch.cuda.synchronize()
+    # the embedding stage at position 0 streams no KV: a walk-only launch decides every tuple from
+    # the caller's margins and queues the survivors; then F1's and F2's gold positions (prep once,
+    # score + walk each) and the final counts
+    assert ko.last_launch_count() == 1 + 3 + 2 + 1
     mg, cg = m.cpu().numpy(), c.cpu().numpy()
     m_or, c_or = oracle.score_workload(wl, np.arange(n))
     m_all = np.concatenate([m_or, emb[:, None, :]], axis=1)
