@@ -195,6 +195,7 @@ struct SoftParams {
   const uint8_t* gold;   // [n_ops][n_tuples] or NULL
   int32_t referenced[kMaxOps];
   double* items;         // workspace [3·S + 1][4][n_tuples]
+  double* partials;      // workspace [4·(3·S + 1)][16]: per-chunk sums of the items
 };
 cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s);
 

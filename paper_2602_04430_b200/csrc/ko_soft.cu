@@ -4,9 +4,9 @@
 // gradient-based optimizer (Adam on the loss of P:424-447) needs every iteration.
 //
 // Per tuple the relaxed cascade is a short chain of scalar operations; derivatives are taken in
-// forward mode with dual numbers, one pass per parameter (3·S ≤ 24), each work item = (tuple,
-// parameter).  Per-item results go to a workspace and are summed per output in a fixed order
-// (fp64), so results are bitwise reproducible.  Equations (same order as oracle/soft.py):
+// forward mode with dual numbers, one pass per parameter (3·S ≤ 24) over stage values computed
+// once (soft_stage_kernel, then soft_items_kernel).  Per-(direction, output, tuple) results go to a workspace and are
+// summed per output in a fixed order (fp64), so results are bitwise reproducible.  Equations (same order as oracle/soft.py):
 //   σ_i = sigmoid(s_i/τ) (finals: 1);  π_i = softmax([m − θ⁺, θ⁻ − m, 0]/τ) (finals: 2-way
 //   sigmoid((m − θ⁺)/τ));  a_i = a + u σ π_acc, r_i = r + u σ π_rej, u = 1 − a − r per op;
 //   cost += σ_i c_i u_{op_i} Π_{o'≠op_i}(1 − r_{o'});  A = Π_o a_o;  TP = Σ A g, FP = Σ A(1−g),
@@ -44,93 +44,142 @@ __device__ __forceinline__ void dsoftmax3(Dual z0, Dual z1, Dual* p0, Dual* p1) 
   *p1 = {q1, q1 * (z1.d - dm)};
 }
 
-__global__ void soft_items_kernel(const __grid_constant__ SoftParams p) {
+// One thread per tuple.  Every stage's relaxed quantities (σ_i, π_acc,i, π_rej,i) and their local
+// derivatives w.r.t. (s_i, θ⁻_i, θ⁺_i) are computed once — all the exp() calls — and kept in
+// registers; then the cheap recurrence runs once per parameter direction (forward mode, dual
+// numbers seeded at that parameter's stage; k = 0: values, k = 1 + 3i + f: field f of stage i).
+// Local derivatives (the closed forms of the dual-number rules):
+//   σ = sigmoid(s/τ):            ∂σ/∂s = σ(1 − σ)/τ                         (finals: σ = 1)
+//   (π_a, π_r) = softmax3((m − θ⁺)/τ, (θ⁻ − m)/τ, 0):
+//       ∂π_a/∂θ⁺ = −π_a(1 − π_a)/τ,  ∂π_r/∂θ⁺ = π_a π_r/τ,
+//       ∂π_a/∂θ⁻ = −π_a π_r/τ,       ∂π_r/∂θ⁻ = π_r(1 − π_r)/τ
+//   finals: π_a = sigmoid((m − θ⁺)/τ), π_r = 1 − π_a: ∂π_a/∂θ⁺ = −π_a(1 − π_a)/τ = −∂π_r/∂θ⁺.
+template <int SM>  // ≥ the plan's stages
+__global__ void soft_tuple_kernel(const __grid_constant__ SoftParams p) {
   const int S = p.plan.n_stages;
-  const int P = 3 * S + 1;  // item k = 0: value pass; k = 1 + 3i + f: derivative w.r.t. field f
-  const int64_t n_items = p.n_tuples * P;
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n_items;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(it / p.n_tuples);
-    const int64_t t = it - (int64_t)k * p.n_tuples;
-    const int seed_stage = k == 0 ? -1 : (k - 1) / 3, seed_field = k == 0 ? -1 : (k - 1) % 3;
-    Dual a[kMaxOps], r[kMaxOps];
-    for (int o = 0; o < kMaxOps; ++o) { a[o] = mk(0.0); r[o] = mk(0.0); }
-    Dual cost = mk(0.0);
-    for (int i = 0; i < S; ++i) {
+  const int P = 3 * S + 1;
+  const double itau = 1.0 / p.tau;
+  const int64_t n = p.n_tuples;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double vs[SM], va[SM], vr[SM], ds[SM], dalo[SM], dahi[SM], drlo[SM], drhi[SM];
+#pragma unroll
+    for (int i = 0; i < SM; ++i) {
+      vs[i] = 1.0; va[i] = vr[i] = ds[i] = dalo[i] = dahi[i] = drlo[i] = drhi[i] = 0.0;
+      if (i >= S) continue;
       const ko_stage& st = p.plan.stage[i];
-      const int o = st.op;
-      const double m = (double)p.margins[((size_t)o * p.n_variants + st.variant) * p.n_tuples + t];
-      const Dual s = mk(p.pick[i], seed_stage == i && seed_field == 0 ? 1.0 : 0.0);
-      const Dual lo = mk((double)st.theta_lo, seed_stage == i && seed_field == 1 ? 1.0 : 0.0);
-      const Dual hi = mk((double)st.theta_hi, seed_stage == i && seed_field == 2 ? 1.0 : 0.0);
-      const double itau = 1.0 / p.tau;
-      Dual sig, pa, pr;
+      const double m = (double)p.margins[((size_t)st.op * p.n_variants + st.variant) * n + t];
+      const double hi = (double)st.theta_hi, lo = (double)st.theta_lo;
       if (st.is_final) {
-        sig = mk(1.0);
-        pa = dsigmoid(itau * (mk(m) - hi));
-        pr = mk(1.0) - pa;
+        const Dual pa = dsigmoid(itau * (mk(m) - mk(hi, 1.0)));  // seeded in θ⁺
+        va[i] = pa.v; vr[i] = 1.0 - pa.v; dahi[i] = pa.d; drhi[i] = -pa.d;
       } else {
-        sig = dsigmoid(itau * s);
-        dsoftmax3(itau * (mk(m) - hi), itau * (lo - mk(m)), &pa, &pr);
+        const Dual sg = dsigmoid(itau * mk(p.pick[i], 1.0));  // seeded in s
+        vs[i] = sg.v; ds[i] = sg.d;
+        Dual pa, pr;
+        dsoftmax3(itau * (mk(m) - mk(hi, 1.0)), itau * (mk(lo) - mk(m)), &pa, &pr);  // θ⁺
+        va[i] = pa.v; vr[i] = pr.v; dahi[i] = pa.d; drhi[i] = pr.d;
+        dsoftmax3(itau * (mk(m) - mk(hi)), itau * (mk(lo, 1.0) - mk(m)), &pa, &pr);  // θ⁻
+        dalo[i] = pa.d; drlo[i] = pr.d;
       }
-      const Dual u = mk(1.0) - a[o] - r[o];
-      Dual alive = mk(1.0);
-      for (int o2 = 0; o2 < p.n_ops; ++o2)
-        if (o2 != o && p.referenced[o2]) alive = alive * (mk(1.0) - r[o2]);
-      cost = cost + p.stage_cost[i] * (sig * u * alive);
-      a[o] = a[o] + u * sig * pa;
-      r[o] = r[o] + u * sig * pr;
     }
-    Dual A = mk(1.0);
     double g = 1.0;
-    for (int o = 0; o < p.n_ops; ++o)
-      if (p.referenced[o]) {
-        A = A * a[o];
-        g *= p.gold ? (double)(p.gold[(size_t)o * p.n_tuples + t] == 1) : 0.0;
+#pragma unroll
+    for (int o = 0; o < kMaxOps; ++o)
+      if (o < p.n_ops && p.referenced[o])
+        g *= p.gold ? (double)(p.gold[(size_t)o * n + t] == 1) : 0.0;
+    for (int k = 0; k < P; ++k) {
+      const int seed_stage = k == 0 ? -1 : (k - 1) / 3, seed_field = k == 0 ? -1 : (k - 1) % 3;
+      Dual a[kMaxOps], r[kMaxOps];
+#pragma unroll
+      for (int o = 0; o < kMaxOps; ++o) { a[o] = mk(0.0); r[o] = mk(0.0); }
+      Dual cost = mk(0.0);
+#pragma unroll
+      for (int i = 0; i < SM; ++i) {
+        if (i >= S) continue;
+        const int o = p.plan.stage[i].op;
+        const bool sd = seed_stage == i;
+        const Dual sig = mk(vs[i], sd && seed_field == 0 ? ds[i] : 0.0);
+        const Dual pa = mk(va[i], sd ? (seed_field == 1 ? dalo[i] : seed_field == 2 ? dahi[i] : 0.0) : 0.0);
+        const Dual pr = mk(vr[i], sd ? (seed_field == 1 ? drlo[i] : seed_field == 2 ? drhi[i] : 0.0) : 0.0);
+        // a / r indexed by compile-time op slots (selects, not a local-memory array)
+        Dual ao = mk(0.0), ro = mk(0.0), alive = mk(1.0);
+#pragma unroll
+        for (int o2 = 0; o2 < kMaxOps; ++o2) {
+          if (o2 == o) { ao = a[o2]; ro = r[o2]; }
+          else if (o2 < p.n_ops && p.referenced[o2]) alive = alive * (mk(1.0) - r[o2]);
+        }
+        const Dual u = mk(1.0) - ao - ro;
+        cost = cost + p.stage_cost[i] * (sig * u * alive);
+        const Dual na = ao + u * sig * pa, nr = ro + u * sig * pr;
+#pragma unroll
+        for (int o2 = 0; o2 < kMaxOps; ++o2)
+          if (o2 == o) { a[o2] = na; r[o2] = nr; }
       }
-    double* dst = p.items + (size_t)k * 4 * p.n_tuples;
-    const bool val = k == 0;
-    dst[0 * p.n_tuples + t] = val ? A.v * g : A.d * g;
-    dst[1 * p.n_tuples + t] = val ? A.v * (1.0 - g) : A.d * (1.0 - g);
-    dst[2 * p.n_tuples + t] = val ? (1.0 - A.v) * g : -A.d * g;
-    dst[3 * p.n_tuples + t] = val ? cost.v : cost.d;
+      Dual A = mk(1.0);
+#pragma unroll
+      for (int o = 0; o < kMaxOps; ++o)
+        if (o < p.n_ops && p.referenced[o]) A = A * a[o];
+      double* dst = p.items + (size_t)k * 4 * n;
+      const bool val = k == 0;
+      dst[0 * n + t] = val ? A.v * g : A.d * g;
+      dst[1 * n + t] = val ? A.v * (1.0 - g) : A.d * (1.0 - g);
+      dst[2 * n + t] = val ? (1.0 - A.v) * g : -A.d * g;
+      dst[3 * n + t] = val ? cost.v : cost.d;
+    }
   }
 }
 
-// one block per output row: fixed-order sum of n values (strided per thread, then a tree)
-// row = 4k + q (item k, quantity q) → out[q] for k = 0, out[4 + q·3S + (k − 1)] otherwise
-__global__ void soft_reduce_kernel(const double* items, int64_t n, double* out, int n_rows, int S) {
+// Fixed-order sums of the items: pass 1, kSoftChunks CTAs per output row each sum one contiguous
+// chunk (8 independent accumulators per thread, then a fixed tree); pass 2 adds a row's chunk
+// sums in chunk order.  Bitwise reproducible.
+constexpr int kSoftChunks = 16;
+__global__ void soft_reduce_kernel(const double* items, int64_t n, double* part, int n_rows) {
   __shared__ double sh[256];
-  const int row = blockIdx.x;
+  const int row = blockIdx.x / kSoftChunks, chunk = blockIdx.x % kSoftChunks;
   if (row >= n_rows) return;
+  const int64_t per = (n + kSoftChunks - 1) / kSoftChunks;
+  const int64_t b0 = chunk * per, b1 = min(n, b0 + per);
   const double* src = items + (size_t)row * n;
-  double acc = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += src[i];
-  sh[threadIdx.x] = acc;
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int64_t i = b0 + threadIdx.x;
+  for (; i + 7 * 256 < b1; i += 8 * 256) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += src[i + u * 256];
+  }
+  for (int u = 0; i < b1; i += 256, ++u) acc[u & 7] += src[i];
+  double a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  sh[threadIdx.x] = a;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
     __syncthreads();
   }
-  const int k = row / 4, q = row % 4;
-  if (threadIdx.x == 0) out[k == 0 ? q : 4 + q * 3 * S + (k - 1)] = sh[0];
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
 
-__global__ void fill_zero_kernel(double* out, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = 0.0;
+__global__ void soft_final_kernel(const double* part, double* out, int n_rows, int S) {
+  for (int row = threadIdx.x; row < n_rows; row += blockDim.x) {
+    double a = 0.0;
+    for (int c = 0; c < kSoftChunks; ++c) a += part[row * kSoftChunks + c];
+    const int k = row / 4, q = row % 4;
+    out[k == 0 ? q : 4 + q * 3 * S + (k - 1)] = a;
+  }
 }
+
 
 }  // namespace
 
 cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s) {
   const int S = p.plan.n_stages;
   const int P = 3 * S + 1;
-  fill_zero_kernel<<<1, 128, 0, s>>>(out, 4 + 12 * S);
-  const int64_t items = p.n_tuples * P;
-  int blocks = (int)std::min<int64_t>((items + 255) / 256, 148 * 16);
+  int blocks = (int)std::min<int64_t>((p.n_tuples + 127) / 128, 148 * 16);
   if (blocks < 1) blocks = 1;
-  soft_items_kernel<<<blocks, 256, 0, s>>>(p);
-  soft_reduce_kernel<<<4 * P, 256, 0, s>>>(p.items, p.n_tuples, out, 4 * P, S);
+  if (S <= 2) soft_tuple_kernel<2><<<blocks, 128, 0, s>>>(p);
+  else if (S <= 4) soft_tuple_kernel<4><<<blocks, 128, 0, s>>>(p);
+  else soft_tuple_kernel<8><<<blocks, 128, 0, s>>>(p);
+  soft_reduce_kernel<<<4 * P * kSoftChunks, 256, 0, s>>>(p.items, p.n_tuples, p.partials, 4 * P);
+  soft_final_kernel<<<1, 128, 0, s>>>(p.partials, out, 4 * P, S);
   return cudaGetLastError();
 }
 
