@@ -93,3 +93,52 @@ def test_random_problem_grid_and_routed(ko, seed):
         m2n, c2n = m2.cpu().numpy(), c2.cpu().numpy()
         parity.assert_margins(m2n, m_or, mask=np.isfinite(m2n))
         parity.assert_counts(cnt2.cpu().numpy(), m_or, c_or, m2n, c2n, [plan], list(classes), gold)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_routed_with_external_stages(ko, seed):
+    """Routed plans mixing external stages (caller-supplied margins, e.g. an embedding filter) at
+    random positions — including first, where position 0 is a walk-only launch — with KV stages:
+    reached margins and counts equal the oracle's."""
+    rng = np.random.default_rng(5000 + seed)
+    geom = Geom(2, 2, 4, 64, 1)
+    n_ops = int(rng.integers(1, 4))
+    classes = tuple([1] * n_ops)
+    lengths = rng.integers(1, 120, size=30).tolist()
+    K, V, ops_h = random_problem(rng, geom, lengths, n_ops=n_ops, classes=classes)
+    pool, indptr, ids, sl = build_pool(K, V, lengths, poison=True, seed=seed)
+    variants = [(int(rng.integers(100, 600)), 1), (1000, 2), (0, 0)]   # last: external
+    ev = len(variants) - 1
+    m_or, c_or = oracle.score(geom, pool, indptr, ids, sl, ops_h, variants[:ev])
+    n = len(lengths)
+    ext = rng.normal(0, 1, size=(n_ops, n)).astype(np.float32)
+    m_all = np.concatenate([m_or, ext[:, None, :].astype(np.float64)], axis=1)
+    c_all = np.concatenate([c_or, np.zeros((n_ops, 1, n), np.int32)], axis=1)
+    plan = []
+    per_op = []
+    for o in range(n_ops):
+        st = []
+        if rng.random() < 0.7:                                   # external stage first
+            lo, hi = sorted(rng.normal(0, 0.7, size=2).tolist())
+            st.append((o, ev, lo, hi, 0))
+        if rng.random() < 0.6:
+            q = np.quantile(m_or[o, 0], [0.3, 0.7])
+            st.append((o, 0, float(q[0]), float(q[1]), 0))
+        th = float(np.quantile(m_or[o, 1], 0.5))
+        st.append((o, 1, th, th, 1))
+        per_op.append(st)
+    while any(per_op):
+        o = int(rng.choice([i for i, st in enumerate(per_op) if st]))
+        plan.append(per_op[o].pop(0))
+    gold = np.stack([(m_or[o, 1] > 0) for o in range(n_ops)]).astype(np.uint8)
+    kv, ops = tensors_to_device(pool, indptr, ids, sl, geom, ops_h)
+    margins = torch.full((n_ops, len(variants), n), float("nan"), device="cuda")
+    margins[:, ev, :] = torch.from_numpy(ext).cuda()
+    m, c, counts = ko.score_batch(kv, ops, variants, margins=margins, plans=[plan],
+                                  gold=torch.from_numpy(gold).cuda())
+    torch.cuda.synchronize()
+    mg, cg = m.cpu().numpy(), c.cpu().numpy()
+    assert np.array_equal(mg[:, ev], ext)                        # external margins untouched
+    kvm = np.isfinite(mg[:, :ev])
+    parity.assert_margins(mg[:, :ev], m_or, mask=kvm)
+    parity.assert_counts(counts.cpu().numpy(), m_all, c_all, mg, cg, [plan], list(classes), gold)
