@@ -63,6 +63,8 @@ def _ops(n=1, classes=1):
     (lambda a: a.update(plans=[[(0, 0, -1.0, 1.0, 1)]] * 2), "final filter", 1),
     (lambda a: a.update(plans=[[(0, 0, 0, 0, 1), (0, 0, -1, 1, 0)]] * 2), "after its final", 1),
     (lambda a: a.update(ws_bytes=16), "workspace", 4),
+    # 16 rows of an 8-class fp32-readout map: 16 W·V entries per row exceed the table packing
+    (lambda a: a.update(ops=_ops(classes=8), kv=_kv(gqa=16)), "W·V tiles", 2),
 ])
 def test_validation_errors_without_gpu(mutate, needle, code):
     import paper_2602_04430_b200 as ko
