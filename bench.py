@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-gb", type=float, default=24.0,
                     help="pinned host memory per rank for the e2e batch")
+    ap.add_argument("--embed-subset", type=float, default=0.0,
+                    help="embed mode: score a sorted random subset (this fraction) of the tuples "
+                         "through tuple_idx (the gathered path) instead of all of them")
     ap.add_argument("--mode", default="pass", choices=["pass", "soft", "embed", "build", "reduce"],
                     help="pass: the hot path (default); soft / embed / build: NEXT-1/3/4 kernels")
     return ap.parse_args()
@@ -536,14 +539,23 @@ def run_next(args):
         di = torch.from_numpy(item.view(np.int16)).cuda().view(torch.bfloat16)
         dq = torch.from_numpy(op.view(np.int16)).cuda().view(torch.bfloat16)
         m = torch.empty((2, 1, n), device="cuda")
-        ms = _time(lambda: ko.embed_scores(di, dq, [0, 1], m, variant=0), args.steps, args.warmup)
-        alg = n * dim * 2 + n * 2 * 4
+        idx, n_sc = None, n
+        if args.embed_subset > 0:          # reached tuples of a cascade: a sorted worklist
+            r = np.random.default_rng(7).random(n) < args.embed_subset
+            idx = torch.from_numpy(np.nonzero(r)[0].astype(np.int32)).cuda()
+            n_sc = int(idx.numel())
+        ms = _time(lambda: ko.embed_scores(di, dq, [0, 1], m, variant=0, tuple_idx=idx),
+                   args.steps, args.warmup)
+        n = n_sc
+        alg = n * dim * 2 + n * 2 * 4 + (n * 4 if idx is not None else 0)
         line = {"mode": "embed", "metric": "embedding-similarity scores / s", "unit": "tuples/s",
                 "value": n / (ms / 1000.0), "ms_per_step": ms,
                 "roofline": {"bound": "hbm", "achieved": alg / (ms / 1000.0) / 1e9, "peak": peak,
                              "unit": "GB/s", "frac": alg / (ms / 1000.0) / 1e9 / peak,
                              "peak_source": peak_src},
-                "config": {"workload": f"{n} tuples x {dim}-d bf16 item embeddings, 2 operators"}}
+                "config": {"workload": f"{n} tuples x {dim}-d bf16 item embeddings, 2 operators"
+                           + (f", gathered via tuple_idx ({args.embed_subset:g} of {len(item)})"
+                              if idx is not None else "")}}
     print(json.dumps(line), flush=True)
 
 

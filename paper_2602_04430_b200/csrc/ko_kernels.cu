@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_
                      : emb_sm;
   uint8_t* ring = base + (size_t)warp * kEmbStages * SB;
   const uint32_t ring_s = smem_u32(ring);
-  if (lane == 0) {
-    for (int s = 0; s < kEmbStages; ++s) mbar_init(&bar[warp][s], 1);
+  if (lane == 0) {  // TM: one arrival (lane 0's expect_tx) + bytes; gathers: one per lane
+    for (int s = 0; s < kEmbStages; ++s) mbar_init(&bar[warp][s], TM ? 1 : 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -573,7 +573,14 @@ __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_
   int64_t next = (int64_t)blockIdx.x * kEmbWarps + warp;  // next block to issue
   uint32_t issued = 0, consumed = 0;
   const uint32_t row_bytes = (uint32_t)dim * 2;
-  auto tuple_of = [&](int64_t w) -> int64_t { return p.tuple_idx ? (int64_t)p.tuple_idx[w] : w; };
+  // gathers: lane r's tuple of the NEXT block to issue, loaded one issue ahead so the index
+  // lookup is off the copy's critical path
+  // (kept as the loaded int32: widening it at the load would wait for the load right there)
+  auto load_tl = [&]() -> int32_t {
+    const int64_t w = next * kEmbRows + lane;
+    return (!TM && next < n_blk && w < n) ? p.tuple_idx[w] : 0;
+  };
+  int32_t tl_next = load_tl();
   auto issue = [&]() {
     const int slot = issued % kEmbStages;
     const int64_t w0 = next * kEmbRows;
@@ -593,22 +600,28 @@ __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_
       next += nw;
       return;
     }
-    // gathered rows: one 1-D bulk copy per row, all issued by lane 0 (a bulk copy takes uniform
-    // operands; lanes issuing their own rows would be serialised by the compiler anyway)
-    const int64_t tl = lane < rows ? tuple_of(w0 + lane) : 0;
-    if (lane == 0) mbar_expect_tx(&bar[warp][slot], row_bytes * rows);
-    for (int r = 0; r < rows; ++r) {
-      const int64_t t = __shfl_sync(0xffffffffu, tl, r);
-      if (lane == 0)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
-            "%2, [%3], %4;" ::"r"(ring_s + slot * SB + r * RS),
-            "l"(p.item_emb + (size_t)t * dim), "r"(row_bytes), "r"(smem_u32(&bar[warp][slot])),
-            "l"(policy)
-            : "memory");
+    // gathered rows: every lane copies 16-byte chunks (cp.async) of the block's rows into the
+    // padded stage, then arrives on the stage's mbarrier when its copies land (.noinc: the
+    // barrier was initialised with one pending arrival per lane)
+    const int cpr = (int)(row_bytes >> 4);  // 16-byte chunks per row (≤ 64)
+    const int32_t tl = tl_next;
+    for (int r = 0; r < rows; ++r) {  // row r: lanes copy chunks lane, lane + 32
+      const uint32_t t = (uint32_t)__shfl_sync(0xffffffffu, tl, r);
+      const uint16_t* src = p.item_emb + (size_t)t * dim;
+      const uint32_t dst = ring_s + slot * SB + r * RS;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int k = lane + 32 * j;
+        if (k < cpr)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * k), "l"(src + 8 * k)
+                       : "memory");
+      }
     }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar[warp][slot]))
+                 : "memory");
     ++issued;
     next += nw;
+    tl_next = load_tl();
   };
   for (int k = 0; k < kEmbStages && next < n_blk; ++k) issue();
   // ldmatrix row address of this lane inside a stage: matrix (lane / 8) = (rows +8·(m&1),
@@ -616,6 +629,12 @@ __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_
   const uint32_t lrow = (uint32_t)((lane & 7) + 8 * ((lane >> 3) & 1)) * RS + 16 * (lane >> 4);
   for (int64_t blk = (int64_t)blockIdx.x * kEmbWarps + warp; blk < n_blk; blk += nw) {
     const int slot = consumed % kEmbStages;
+    // output tuples of rows g, g + 8 (gathers: loaded before the wait, off the epilogue's path)
+    const int64_t w0 = blk * kEmbRows;
+    int32_t tout[2];  // int32 until used (see load_tl)
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr)
+      tout[hr] = w0 + g + 8 * hr < n ? (p.tuple_idx ? p.tuple_idx[w0 + g + 8 * hr] : (int32_t)0) : 0;
     mbar_wait(&bar[warp][slot], (consumed / kEmbStages) & 1u);
     const uint32_t st = ring_s + slot * SB + (TM ? 0u : lrow);
     // two accumulator sets (even / odd k-steps) halve the MMA dependency chains
@@ -654,12 +673,11 @@ __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_
     const float gsel1 = (g & 1) ? g1[0][3] : g1[0][2];
     const float n0 = __shfl_sync(0xffffffffu, gsel0, 4 * g + (g >> 1));
     const float n1 = __shfl_sync(0xffffffffu, gsel1, 4 * g + (g >> 1));
-    const int64_t w0 = blk * kEmbRows;
 #pragma unroll
     for (int hr = 0; hr < 2; ++hr) {
       const int64_t w = w0 + g + 8 * hr;
       if (w >= n) continue;
-      const int64_t t = tuple_of(w);
+      const int64_t t = p.tuple_idx ? (int64_t)(uint32_t)tout[hr] : w;
       const float n2 = hr ? n1 : n0;
       const float rn = n2 > 0.f ? rsqrtf(n2) : 0.f;  // 1/‖x‖ (≤ 2 ulp); 0 ⇒ cosine 0
 #pragma unroll

@@ -45,6 +45,27 @@ def test_embed_scores_parity(ko, dim):
     assert np.count_nonzero(g2) == 6
 
 
+@pytest.mark.parametrize("dim", [64, 128, 192, 256, 512])
+def test_embed_scores_gathered(ko, dim):
+    """tuple_idx path (per-lane 16-byte copies into padded rows): many full 16-row blocks plus a
+    ragged tail, unsorted and repeated indices; entries outside the subset stay untouched."""
+    wl = workloads.get("C5")
+    n = 4099
+    item, op = wl.spec.embeddings(3, n, dim)
+    exp = oracle.embed_scores(item, op)
+    rng = np.random.default_rng(dim)
+    sub = rng.choice(n, size=2477, replace=False).astype(np.int32)
+    sub = np.concatenate([sub, sub[:5]])              # repeats write the same value twice
+    m = torch.full((2, 1, n), -9.0, device="cuda")
+    ko.embed_scores(_dev_bits(item), _dev_bits(op), [0, 1], m, variant=0,
+                    tuple_idx=torch.from_numpy(sub).cuda())
+    torch.cuda.synchronize()
+    got = m.cpu().numpy()[:, 0, :]
+    assert np.abs(got[:, sub] - exp[:, sub]).max() < 1e-5
+    rest = np.setdiff1d(np.arange(n), sub)
+    assert np.all(got[:, rest] == -9.0)
+
+
 def test_embedding_first_stage_cascade(ko):
     """C5-shaped cascade: [embedding stage (external) → KV gold] per filter, routed and grid."""
     wl = workloads.get("C5")
