@@ -871,6 +871,7 @@ ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, con
   bp.inv_sqrt_d = 1.0 / std::sqrt((double)src->head_dim);
   bp.inv_2d = 1.0 / (2.0 * (double)src->head_dim);
   KO_LAUNCH(ko::launch_build(bp, (cudaStream_t)stream));
+  ++g_launches;  // launch_build: two kernels (short / long tuples)
   return KO_OK;
 }
 

@@ -8,6 +8,9 @@
 //      one rounding per operation (__dmul_rn/__dadd_rn: no fused multiply-add), so the order is
 //      decided exactly as the oracle decides it;
 //   2. bitonic sort of (s desc, index asc) in shared memory (L ≤ 4096);
+// Two launches sized by token count: units with L ≤ 1024 go to a kernel whose ~22 KB of shared
+// memory lets 6-7 CTAs share an SM (their score / sort / gather phases overlap each other's memory
+// traffic); the rare longer ones to the 4096-token kernel (51 KB).  Each skips the other's units.
 //   3. gather: the K and V rows of rank r go to slot r % 16 of logical page r / 16 of the
 //      destination CSR, 16-byte copies.
 #include <cuda_runtime.h>
@@ -15,6 +18,7 @@
 
 #include <algorithm>
 
+#include "ko_device.cuh"
 #include "ko_internal.h"
 
 namespace ko {
@@ -22,6 +26,11 @@ namespace {
 
 constexpr int kBuildThreads = 256;
 constexpr int kBuildMaxTokens = 4096;
+constexpr int kBuildSmallTokens = 1024;
+// sort keys (doubles) of a MAXT kernel; ≥ 2048 so that, reused as the gather stage, one pass moves
+// ≥ 32 ranks at head_dim 128
+template <int MAXT>
+__host__ __device__ constexpr int key_slots() { return MAXT > 2048 ? MAXT : 2048; }
 
 __device__ __forceinline__ double bf16_to_double(uint16_t b) {
   return (double)__uint_as_float((uint32_t)b << 16);
@@ -32,11 +41,12 @@ __device__ __forceinline__ bool precedes(double ka, int ia, double kb, int ib) {
   return ka > kb || (ka == kb && ia < ib);
 }
 
+template <int MAXT, int MINT>  // this kernel's units: MINT < L ≤ MAXT
 __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_constant__ BuildParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* key = reinterpret_cast<double*>(smem);                  // [N]
-  int* idx = reinterpret_cast<int*>(key + kBuildMaxTokens);       // [N]
-  double* s_mu = reinterpret_cast<double*>(idx + kBuildMaxTokens);  // [D] (exact fp32 → fp64)
+  double* key = reinterpret_cast<double*>(smem);                  // [key_slots]
+  int* idx = reinterpret_cast<int*>(key + key_slots<MAXT>());     // [MAXT]
+  double* s_mu = reinterpret_cast<double*>(idx + MAXT);           // [D] (exact fp32 → fp64)
   double* s_s2 = s_mu + p.head_dim;                                 // [D]
   const int D = p.head_dim, H = p.n_kv_heads, Lyr = p.n_layers;
   const int64_t n_units = p.n_tuples * Lyr * H;
@@ -44,7 +54,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
     const int64_t t = u / (Lyr * H);
     const int l = (int)((u / H) % Lyr), h = (int)(u % H);
     const int L = p.seq_len[t];
-    if (L < 1 || L > kBuildMaxTokens) continue;  // documented limit (device data: skipped)
+    if (L <= MINT || L > MAXT) continue;  // the other launch's (or > 4096: documented, skipped)
     __syncthreads();
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
       s_mu[d] = (double)p.mu[((size_t)l * H + h) * D + d];
@@ -107,7 +117,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
     const int chunks = D / 8;  // a power of two (D ∈ {64, 128}): shifts, not divisions
     const int cs = chunks == 16 ? 4 : 3;
     const int per_rank = 2 * chunks;                         // K and V row chunks of one rank
-    const int ranks_pass = (kBuildMaxTokens * (int)sizeof(double)) / (per_rank * 16);
+    const int ranks_pass = (key_slots<MAXT>() * (int)sizeof(double)) / (per_rank * 16);
     const uint32_t stage = (uint32_t)__cvta_generic_to_shared(key);
     __syncthreads();  // every thread is done with key[] (the sort's last phase)
     for (int r0 = 0; r0 < L; r0 += ranks_pass) {
@@ -132,27 +142,31 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
   }
 }
 
-}  // namespace
-
+template <int MAXT>
 size_t build_smem_bytes(int head_dim) {
-  return (size_t)kBuildMaxTokens * (sizeof(double) + sizeof(int)) + 2 * sizeof(double) * head_dim;
+  return (size_t)key_slots<MAXT>() * sizeof(double) + (size_t)MAXT * sizeof(int) +
+         2 * sizeof(double) * head_dim;
 }
 
-cudaError_t launch_build(const BuildParams& p, cudaStream_t s) {
-  const size_t smem = build_smem_bytes(p.head_dim);
-  static bool attr = false;
-  if (!attr) {  // sized for the largest head_dim once
-    cudaFuncSetAttribute(build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)build_smem_bytes(128));
-    attr = true;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+template <int MAXT, int MINT>
+cudaError_t launch_build_t(const BuildParams& p, cudaStream_t s) {
+  auto kern = build_kernel<MAXT, MINT>;
+  const size_t smem = build_smem_bytes<MAXT>(p.head_dim);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBuildThreads, smem);
   const int64_t units = p.n_tuples * p.n_layers * p.n_kv_heads;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)sms * 4));
-  build_kernel<<<grid, kBuildThreads, smem, s>>>(p);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)num_sms() * std::max(occ, 1)));
+  kern<<<grid, kBuildThreads, smem, s>>>(p);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_build(const BuildParams& p, cudaStream_t s) {  // 2 launches
+  cudaError_t e = launch_build_t<kBuildSmallTokens, 0>(p, s);
+  if (e != cudaSuccess) return e;
+  return launch_build_t<kBuildMaxTokens, kBuildSmallTokens>(p, s);
 }
 
 }  // namespace ko

@@ -34,7 +34,7 @@ def _valid_slots_equal(a, b, indptr, ids, sl):
 def test_build_matches_oracle(ko, D):
     rng = np.random.default_rng(D)
     geom = Geom(2, 2, 1, D, 1)
-    lengths = [1, 15, 16, 17, 300, 4096]
+    lengths = [1, 15, 16, 17, 300, 1024, 1025, 2049, 4096]   # both launches, their boundary
     K, V, _ = random_problem(rng, geom, lengths)
     pool, indptr, ids, sl = build_pool(K, V, lengths, placement="shuffle", seed=1, poison=True)
     mu = rng.normal(0, 1, size=(2, 2, D)).astype(np.float32)
