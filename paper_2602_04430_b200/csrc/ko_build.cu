@@ -95,9 +95,9 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
     // bitonic sort: final order has precedes(i, i+1)
     for (int k = 2; k <= N; k <<= 1)
       for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < N; i += blockDim.x) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
+        for (int q = threadIdx.x; q < (N >> 1); q += blockDim.x) {  // one thread per pair
+          const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1)), ixj = i | j;  // bit j of i clear
+          {
             const bool up = (i & k) == 0;  // this pair must end in `precedes` order
             const double ka = key[i], kb = key[ixj];
             const int ia = idx[i], ib = idx[ixj];
