@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
       const int64_t page = p.src_ids[pbase + (i >> 4)];
       return p.src_pool + (size_t)page * p.page_elems + (which ? off_v : off_k) + (i & 15) * D;
     };
-    int N = 1;
+    int N = 64;  // ≥ one warp segment (padding sorts last)
     while (N < L) N <<= 1;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       if (i < L) {
@@ -92,24 +92,65 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
       }
     }
     __syncthreads();
-    // bitonic sort: final order has precedes(i, i+1)
-    for (int k = 2; k <= N; k <<= 1)
-      for (int j = k >> 1; j > 0; j >>= 1) {
+    // bitonic sort: final order has precedes(i, i+1).  Phases whose pairs lie inside a 64-element
+    // segment (j ≤ 32) run in registers, one warp per segment, lane holding elements lane and
+    // lane + 32 (j = 32: in-lane, j < 32: shuffles); only the j ≥ 64 phases go through shared
+    // memory with a CTA barrier — 6 barriers at N = 512 instead of 45.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n_warps = blockDim.x >> 5;
+    auto seg_phases = [&](int k_lo, int k_hi, int j_top) {  // levels k_lo..k_hi, first j ≤ j_top
+      for (int seg = warp; seg < (N >> 6); seg += n_warps) {
+        const int base = seg << 6;
+        double kk[2] = {key[base + lane], key[base + lane + 32]};
+        int ii[2] = {idx[base + lane], idx[base + lane + 32]};
+        for (int k = k_lo; k <= k_hi; k <<= 1)
+          for (int j = min(k >> 1, j_top); j > 0; j >>= 1) {
+            if (j == 32) {  // pair (lane, lane + 32): both here, element lane is the lower
+              const bool up = ((base + lane) & k) == 0;
+              const bool swap = up ? precedes(kk[1], ii[1], kk[0], ii[0])
+                                   : precedes(kk[0], ii[0], kk[1], ii[1]);
+              if (swap) {
+                const double tk = kk[0]; kk[0] = kk[1]; kk[1] = tk;
+                const int ti = ii[0]; ii[0] = ii[1]; ii[1] = ti;
+              }
+            } else {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int i = base + lane + 32 * h;
+                const double ko = __shfl_xor_sync(0xffffffffu, kk[h], j);
+                const int io = __shfl_xor_sync(0xffffffffu, ii[h], j);
+                const bool up = (i & k) == 0, lower = (lane & j) == 0;
+                // the lower position keeps the element that comes first (up) / second (down)
+                const bool other_first = precedes(ko, io, kk[h], ii[h]);
+                if (lower == (up == other_first) && (ko != kk[h] || io != ii[h])) {
+                  kk[h] = ko;
+                  ii[h] = io;
+                }
+              }
+            }
+          }
+        key[base + lane] = kk[0]; key[base + lane + 32] = kk[1];
+        idx[base + lane] = ii[0]; idx[base + lane + 32] = ii[1];
+      }
+      __syncthreads();
+    };
+    seg_phases(2, 64, 32);  // every level up to 64 lies inside segments
+    for (int k = 128; k <= N; k <<= 1) {
+      for (int j = k >> 1; j >= 64; j >>= 1) {
         for (int q = threadIdx.x; q < (N >> 1); q += blockDim.x) {  // one thread per pair
           const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1)), ixj = i | j;  // bit j of i clear
-          {
-            const bool up = (i & k) == 0;  // this pair must end in `precedes` order
-            const double ka = key[i], kb = key[ixj];
-            const int ia = idx[i], ib = idx[ixj];
-            const bool swap = up ? precedes(kb, ib, ka, ia) : precedes(ka, ia, kb, ib);
-            if (swap) {
-              key[i] = kb; key[ixj] = ka;
-              idx[i] = ib; idx[ixj] = ia;
-            }
+          const bool up = (i & k) == 0;  // this pair must end in `precedes` order
+          const double ka = key[i], kb = key[ixj];
+          const int ia = idx[i], ib = idx[ixj];
+          const bool swap = up ? precedes(kb, ib, ka, ia) : precedes(ka, ia, kb, ib);
+          if (swap) {
+            key[i] = kb; key[ixj] = ka;
+            idx[i] = ib; idx[ixj] = ia;
           }
         }
         __syncthreads();
       }
+      seg_phases(k, k, 32);
+    }
     // gather: rank r ← token idx[r].  The sort keys are dead now, so their 32 KB stage the copy:
     // per pass every thread issues its 16-byte chunks of the next block of ranks as cp.async
     // (global → shared, nothing held in registers, all in flight at once), then writes them to

@@ -69,3 +69,32 @@ def test_build_on_generated_workload(ko):
     torch.cuda.synchronize()
     got = dst.view(torch.int16).cpu().numpy().view(np.uint16)
     assert _valid_slots_equal(got, exp, indptr, ids, sl)
+
+
+def test_build_ties_keep_source_order(ko):
+    """mu = sigma2 = 0: every score ties, so (ties: lower source index first, ko.h) the built
+    store is the source order — exercises every tie-break branch of the register and shared
+    memory sort phases; plus duplicated rows mixed with distinct ones, vs the oracle."""
+    rng = np.random.default_rng(11)
+    geom = Geom(1, 2, 1, 64, 1)
+    lengths = [5, 64, 65, 700, 1500]
+    K, V, _ = random_problem(rng, geom, lengths)
+    for t in range(len(lengths)):                  # duplicate rows: equal scores, distinct tokens
+        K[t][..., 1::3, :] = K[t][..., :1, :]
+    pool, indptr, ids, sl = build_pool(K, V, lengths, placement="shuffle", seed=4, poison=True)
+    kv, _ = tensors_to_device(pool, indptr, ids, sl, geom,
+                              [dict(n_classes=1, q=np.zeros((1, 2, 1, 64), np.uint16),
+                                    w=np.zeros((1, 1, 2, 1, 64), np.float32),
+                                    b=np.zeros(1, np.float32))])
+    for mu_scale in (0.0, 1.0):
+        mu = (mu_scale * rng.normal(0, 1, size=(1, 2, 64))).astype(np.float32)
+        s2 = (mu_scale * rng.uniform(0, 1, size=(1, 2, 64))).astype(np.float32)
+        exp = oracle.build_order(geom, pool, indptr, ids, sl, mu, s2, ids)
+        if mu_scale == 0.0:
+            assert _valid_slots_equal(exp, pool, indptr, ids, sl)   # identity order
+        dst = torch.zeros_like(kv.pool)
+        ko.build_importance_order(kv, torch.from_numpy(mu).cuda(), torch.from_numpy(s2).cuda(),
+                                  dst, kv.page_ids)
+        torch.cuda.synchronize()
+        got = dst.view(torch.int16).cpu().numpy().view(np.uint16)
+        assert _valid_slots_equal(got, exp, indptr, ids, sl)
