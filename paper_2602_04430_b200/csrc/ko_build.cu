@@ -8,11 +8,11 @@
 //      one rounding per operation (__dmul_rn/__dadd_rn: no fused multiply-add), so the order is
 //      decided exactly as the oracle decides it;
 //   2. bitonic sort of (s desc, index asc) in shared memory (L ≤ 4096);
-// Two launches sized by token count: units with L ≤ 1024 go to a kernel whose ~22 KB of shared
-// memory lets 6-7 CTAs share an SM (their score / sort / gather phases overlap each other's memory
+// Two launches sized by token count: units with L ≤ 1024 go to a kernel with ~14 KB of shared
+// memory, so several CTAs share an SM (their score / sort / gather phases overlap each other's memory
 // traffic); the rare longer ones to the 4096-token kernel (51 KB).  Each skips the other's units.
 //   3. gather: the K and V rows of rank r go to slot r % 16 of logical page r / 16 of the
-//      destination CSR, 16-byte copies.
+//      destination CSR, 16-byte copies through registers.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -27,10 +27,9 @@ namespace {
 constexpr int kBuildThreads = 256;
 constexpr int kBuildMaxTokens = 4096;
 constexpr int kBuildSmallTokens = 1024;
-// sort keys (doubles) of a MAXT kernel; ≥ 2048 so that, reused as the gather stage, one pass moves
-// ≥ 32 ranks at head_dim 128
+// sort keys (doubles) of a MAXT kernel
 template <int MAXT>
-__host__ __device__ constexpr int key_slots() { return MAXT > 2048 ? MAXT : 2048; }
+__host__ __device__ constexpr int key_slots() { return MAXT; }
 
 __device__ __forceinline__ double bf16_to_double(uint16_t b) {
   return (double)__uint_as_float((uint32_t)b << 16);
@@ -151,34 +150,34 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
       }
       seg_phases(k, k, 32);
     }
-    // gather: rank r ← token idx[r].  The sort keys are dead now, so their 32 KB stage the copy:
-    // per pass every thread issues its 16-byte chunks of the next block of ranks as cp.async
-    // (global → shared, nothing held in registers, all in flight at once), then writes them to
-    // the destination pages.
+    // gather: rank r ← token idx[r], 16-byte chunks through registers — each thread issues 4
+    // loads, then stores them; no shared-memory stage and no CTA barrier, so warps stream
+    // independently (the barrier after a staged pass was the top stall: ncu, 20 % of samples)
     const int chunks = D / 8;  // a power of two (D ∈ {64, 128}): shifts, not divisions
     const int cs = chunks == 16 ? 4 : 3;
-    const int per_rank = 2 * chunks;                         // K and V row chunks of one rank
-    const int ranks_pass = (key_slots<MAXT>() * (int)sizeof(double)) / (per_rank * 16);
-    const uint32_t stage = (uint32_t)__cvta_generic_to_shared(key);
-    __syncthreads();  // every thread is done with key[] (the sort's last phase)
-    for (int r0 = 0; r0 < L; r0 += ranks_pass) {
-      const int n_c = min(ranks_pass, L - r0) * per_rank;
-      for (int w = threadIdx.x; w < n_c; w += blockDim.x) {
-        const int r = r0 + (w >> (cs + 1)), which = (w >> cs) & 1, ch = w & (chunks - 1);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(stage + 16u * (uint32_t)w),
-                     "l"(src_row(which, idx[r]) + ch * 8)
-                     : "memory");
+    const int n_c = L * 2 * chunks;  // K and V row chunks of every rank
+    constexpr int kU = 4;  // A/B: 2 → 8.49 ms, 4 → 7.58 ms, 8 → 7.77 ms (C2, 2000 tuples)
+    for (int w0 = threadIdx.x; w0 < n_c; w0 += kU * blockDim.x) {
+      uint4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int w = w0 + u * blockDim.x;
+        if (w < n_c) {
+          const int r = w >> (cs + 1), which = (w >> cs) & 1, ch = w & (chunks - 1);
+          v[u] = __ldcs(reinterpret_cast<const uint4*>(src_row(which, idx[r]) + ch * 8));
+        }
       }
-      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-      __syncthreads();
-      for (int w = threadIdx.x; w < n_c; w += blockDim.x) {
-        const int r = r0 + (w >> (cs + 1)), which = (w >> cs) & 1, ch = w & (chunks - 1);
-        const int64_t page = p.dst_ids[pbase + (r >> 4)];
-        uint16_t* dst = p.dst_pool + (size_t)page * p.page_elems + (which ? off_v : off_k) +
-                        (r & 15) * D + ch * 8;
-        *reinterpret_cast<uint4*>(dst) = reinterpret_cast<const uint4*>(key)[w];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int w = w0 + u * blockDim.x;
+        if (w < n_c) {
+          const int r = w >> (cs + 1), which = (w >> cs) & 1, ch = w & (chunks - 1);
+          const int64_t page = p.dst_ids[pbase + (r >> 4)];
+          uint16_t* dst = p.dst_pool + (size_t)page * p.page_elems + (which ? off_v : off_k) +
+                          (r & 15) * D + ch * 8;
+          __stcs(reinterpret_cast<uint4*>(dst), v[u]);
+        }
       }
-      __syncthreads();  // the stage is reused by the next pass
     }
   }
 }
