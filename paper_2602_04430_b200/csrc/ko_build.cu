@@ -73,14 +73,20 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
       if (i < L) {
         const uint16_t* k = src_row(0, i);
         double a = 0.0, b = 0.0;
-        for (int d = 0; d < D; d += 8) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(k + d));
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        for (int d0 = 0; d0 < D; d0 += 32) {  // 4 row loads in flight, then their 32 terms in order
+          uint4 vv[4];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const double x = bf16_to_double((uint16_t)(e & 1 ? w[e >> 1] >> 16 : w[e >> 1] & 0xFFFFu));
-            a = __dadd_rn(a, __dmul_rn(s_mu[d + e], x));
-            b = __dadd_rn(b, __dmul_rn(s_s2[d + e], __dmul_rn(x, x)));
+          for (int c = 0; c < 4; ++c) vv[c] = __ldg(reinterpret_cast<const uint4*>(k + d0 + 8 * c));
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int d = d0 + 8 * c;
+            const uint32_t w[4] = {vv[c].x, vv[c].y, vv[c].z, vv[c].w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const double x = bf16_to_double((uint16_t)(e & 1 ? w[e >> 1] >> 16 : w[e >> 1] & 0xFFFFu));
+              a = __dadd_rn(a, __dmul_rn(s_mu[d + e], x));
+              b = __dadd_rn(b, __dmul_rn(s_s2[d + e], __dmul_rn(x, x)));
+            }
           }
         }
         key[i] = __dadd_rn(__dmul_rn(a, p.inv_sqrt_d), __dmul_rn(b, p.inv_2d));
