@@ -48,6 +48,7 @@ def test_build_matches_oracle(ko, D):
     dst = torch.zeros_like(kv.pool)
     ko.build_importance_order(kv, torch.from_numpy(mu).cuda(), torch.from_numpy(s2).cuda(), dst,
                               torch.from_numpy(dst_ids).cuda())
+    assert ko.last_launch_count() == 2                    # short- and long-tuple kernels
     torch.cuda.synchronize()
     got = dst.view(torch.int16).cpu().numpy().view(np.uint16)
     assert _valid_slots_equal(got, exp, indptr, dst_ids, sl)
