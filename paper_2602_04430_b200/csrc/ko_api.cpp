@@ -922,11 +922,15 @@ ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const do
                             align256(sizeof(double) * (size_t)(3 * plan->n_stages + 1) * 4 *
                                      (size_t)std::max<int64_t>(n_tuples, 1)));
   KO_LAUNCH(ko::launch_soft(sp, out, (cudaStream_t)stream));
+  g_launches += 2;  // launch_soft: three kernels (per-tuple items, chunk sums, in-order final sum)
   return KO_OK;
 }
 
 // ---- Bayesian lower bound (host): I^{-1}(1 − α; 1 + a, 1 + b) -------------------------------
-// Regularized incomplete beta by the continued fraction (modified Lentz), inverse by bisection.
+// Regularized incomplete beta by its continued fraction evaluated with the modified Lentz method
+// (textbook algorithm: W. H. Press et al., Numerical Recipes, 3rd ed., §6.4 "Incomplete Beta
+// Function", routine betacf, whose variable names this follows; SPEC S:134 prescribes the same
+// method with the symmetry split at x = (a+1)/(a+b+2)); inverse by bisection.
 static double betacf(double a, double b, double x) {
   const double tiny = 1e-300, eps = 1e-16;
   double qab = a + b, qap = a + 1.0, qam = a - 1.0;

@@ -2,6 +2,7 @@
 // evaluation, counters, mbarrier / TMA / shared-memory primitives).  Internal (not the ABI).
 #pragma once
 
+#include <atomic>
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
@@ -174,13 +175,17 @@ struct Ring {
   static constexpr int kSmemBytes = (kThreads / 32) * kWarpBytes + 1024;  // + alignment slack
 };
 
+// SM count of the CURRENT device, cached per device ordinal (a process may drive several GPUs)
 inline int num_sms() {
-  static int n = 0;
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 63;
+  int n = cache[dev].load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }

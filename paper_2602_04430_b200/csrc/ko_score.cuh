@@ -578,13 +578,19 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 
 template <int D, int CPR, int NT>
 cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t s) {
-  static int occ = 0;
+  // the smem attribute and the occupancy are per device: cached per device ordinal
+  static std::atomic<int> occ_of[64];
   constexpr int smem = Ring<D>::kSmemBytes;
   auto* kern = ko_score_kernel<D, CPR, NT>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 63;
+  int occ = occ_of[dev].load(std::memory_order_relaxed);
   if (!occ) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
     if (occ < 1) occ = 1;
+    occ_of[dev].store(occ, std::memory_order_relaxed);
   }
   const int64_t warps_needed = max_units > 0 ? max_units : 1;
   int64_t grid = (int64_t)num_sms() * occ;
