@@ -61,7 +61,7 @@ def lib():
                                    ctypes.c_int64, P, P, P, ctypes.c_int32, ctypes.c_int32]
         L.oracle_score.restype = ctypes.c_int
         L.oracle_run_plans.argtypes = [P, ctypes.c_int32, P, P, P, ctypes.c_int32, ctypes.c_int32,
-                                       ctypes.c_int64, P, P, P]
+                                       ctypes.c_int64, P, P, P, P]
         L.oracle_run_plans.restype = ctypes.c_int
         L.oracle_build_order.argtypes = [ctypes.POINTER(OrKV), P, P, P, P, ctypes.c_int32]
         L.oracle_build_order.restype = ctypes.c_int
@@ -125,10 +125,18 @@ def score(geom, pool: np.ndarray, indptr: np.ndarray, page_ids: np.ndarray, seq_
     return margins, classes
 
 
+STAGE_NOT_REACHED, STAGE_ACCEPT, STAGE_REJECT, STAGE_UNSURE, STAGE_RESOLVED = 0, 1, 2, 3, 4
+
+
 def run_plans(plans: Sequence[Sequence[Tuple]], margins: np.ndarray, classes: np.ndarray,
               n_classes: Sequence[int], gold: Optional[np.ndarray] = None,
-              want_alive: bool = False):
-    """Counts int64 [n_plans][37] (TP, FP, FN, n_out, n_gold, per-stage n_in/acc/rej/uns)."""
+              want_alive: bool = False, want_stages: bool = False):
+    """Counts int64 [n_plans][37] (TP, FP, FN, n_out, n_gold, per-stage n_in/acc/rej/uns).
+
+    want_alive: also return alive uint8 [n_plans][n] (1 = tuple in P_o).
+    want_stages: also return the per-tuple stage outcomes int8 [n_plans][MAX_STAGES][n]
+    (STAGE_NOT_REACHED / ACCEPT / REJECT / UNSURE / RESOLVED; Eqs. accept-i / reject-i /
+    unsure-i).  Returns counts, then alive, then stages, for the ones requested."""
     margins = np.ascontiguousarray(margins, np.float64)
     classes = np.ascontiguousarray(classes, np.int32)
     n_ops, n_var, n = margins.shape
@@ -136,14 +144,14 @@ def run_plans(plans: Sequence[Sequence[Tuple]], margins: np.ndarray, classes: np
     g = None if gold is None else np.ascontiguousarray(gold, np.uint8)
     counts = np.zeros((len(plans), COUNTS_PER_PLAN), np.int64)
     alive = np.zeros((len(plans), n), np.uint8) if want_alive else None
+    stages = np.zeros((len(plans), MAX_STAGES, n), np.int8) if want_stages else None
     parr = make_plans(plans)
     rc = lib().oracle_run_plans(parr, len(plans), _p(margins), _p(classes), _p(nc), n_ops, n_var,
-                                n, _p(g), _p(counts), _p(alive))
+                                n, _p(g), _p(counts), _p(alive), _p(stages))
     if rc != 0:
         raise ValueError("oracle_run_plans: invalid plan")
-    if want_alive:
-        return counts, alive
-    return counts
+    out = (counts,) + ((alive,) if want_alive else ()) + ((stages,) if want_stages else ())
+    return out if len(out) > 1 else counts
 
 
 def beta_lower_bound(a: int, b: int, alpha: float) -> float:

@@ -201,10 +201,12 @@ int oracle_score(const or_kv* kv, const or_op* ops, int32_t n_ops, const or_vari
 // Steps 6–9.  margins/classes [n_ops][n_variants][n] (fp64), n_classes[n_ops], gold [n_ops][n]
 // (filters 0/1, maps class) or NULL.  counts [n_plans][OR_COUNTS_PER_PLAN] are ACCUMULATED.
 // final_alive (optional) [n_plans][n] receives the end state (1 = in P_o).
+// stage_out (optional) [n_plans][OR_MAX_STAGES][n] receives each stage's outcome per tuple:
+// 0 = not reached (unsure_{t,i-1} = 0), 1 = accept, 2 = reject, 3 = unsure, 4 = map resolved.
 int oracle_run_plans(const or_plan* plans, int32_t n_plans, const double* margins,
                      const int32_t* classes, const int32_t* n_classes, int32_t n_ops,
                      int32_t n_variants, int64_t n, const uint8_t* gold, int64_t* counts,
-                     uint8_t* final_alive) {
+                     uint8_t* final_alive, int8_t* stage_out) {
   for (int32_t g = 0; g < n_plans; ++g) {
     const or_plan* P = &plans[g];
     if (P->n_stages < 1 || P->n_stages > OR_MAX_STAGES) return 1;
@@ -224,10 +226,13 @@ int oracle_run_plans(const or_plan* plans, int32_t n_plans, const double* margin
       for (int s = 0; s < P->n_stages; ++s) {
         const or_stage* st = &P->stage[s];
         const int o = st->op;
+        int8_t* so = stage_out ? stage_out + ((size_t)g * OR_MAX_STAGES + s) * n + t : nullptr;
+        if (so) *so = 0;
         if (!(alive && status[o] == 0)) continue;  // not reached: unsure_{t,i-1} = 0
         cnt[5 + 4 * s] += 1;                        // n_in
         const size_t idx = ((size_t)o * n_variants + st->variant) * n + t;
         const int dcs = decide(margins[idx], st, n_classes[o]);
+        if (so) *so = dcs == D_ACCEPT ? 1 : dcs == D_REJECT ? 2 : dcs == D_RESOLVED ? 4 : 3;
         if (dcs == D_ACCEPT) { status[o] = 1; cnt[6 + 4 * s] += 1; }
         else if (dcs == D_RESOLVED) { status[o] = 1; cls[o] = classes[idx]; cnt[6 + 4 * s] += 1; }
         else if (dcs == D_REJECT) { alive = false; status[o] = 2; cnt[7 + 4 * s] += 1; }

@@ -40,6 +40,8 @@ def brute_force_counts(plan_ops, finals, outcomes, gold):
     ops = sorted(set(plan_ops))
     n_in = [0] * S; n_acc = [0] * S; n_rej = [0] * S; n_uns = [0] * S
     tp = n_out = n_gold = 0
+    codes = np.zeros((S, len(outcomes)), np.int8)      # per-tuple stage outcome (0 = not reached)
+    alive = np.zeros(len(outcomes), np.uint8)
     for t, dec in enumerate(outcomes):
         def state(o, upto):
             idx = [s for s in range(upto) if plan_ops[s] == o]
@@ -52,13 +54,15 @@ def brute_force_counts(plan_ops, finals, outcomes, gold):
                 n_in[s] += 1
                 d = dec[s]
                 n_acc[s] += d == ACC; n_rej[s] += d == REJ; n_uns[s] += d == UNS
+                codes[s, t] = {ACC: 1, REJ: 2, UNS: 3}[d]
         in_out = all(state(o, S)[0] == 1 for o in ops)      # conjunctive AND of each cascade
+        alive[t] = in_out
         in_gold = all(gold[t][o] == 1 for o in ops)
         n_out += in_out; n_gold += in_gold; tp += in_out and in_gold
     row = [tp, n_out - tp, n_gold - tp, n_out, n_gold]
     for s in range(S):
         row += [n_in[s], n_acc[s], n_rej[s], n_uns[s]]
-    return row
+    return row, codes, alive
 
 
 PLAN_SHAPES = [
@@ -99,10 +103,15 @@ def test_routing_brute_force(plan_ops):
             g[o, t] = gold[t][o]
     plan = [(plan_ops[s], s, 0.0 if finals[s] else -1.0, 0.0 if finals[s] else 1.0, int(finals[s]))
             for s in range(S)]
-    counts = oracle.run_plans([plan], margins, classes, [1] * n_ops, g)
-    expect = brute_force_counts(plan_ops, finals, outcomes, gold)
+    counts, alive, stages = oracle.run_plans([plan], margins, classes, [1] * n_ops, g,
+                                             want_alive=True, want_stages=True)
+    expect, codes, alive_bf = brute_force_counts(plan_ops, finals, outcomes, gold)
     assert list(counts[0, :len(expect)]) == expect
     assert not counts[0, len(expect):].any()
+    # per-tuple decisions: each stage's outcome (reached or not) and P_o membership
+    assert np.array_equal(stages[0, :S], codes)
+    assert not stages[0, S:].any()
+    assert np.array_equal(alive[0], alive_bf)
 
 
 def test_count_identities_random():
@@ -173,6 +182,10 @@ def test_threshold_boundaries_strict():
                          np.zeros(m.shape, np.int32), [1], want_alive=True)
     counts, alive = c
     assert counts[0, 5:9].tolist() == [5, 1, 1, 3]          # n_in, acc, rej, uns
+    st = oracle.run_plans([[(0, 0, float(lo), float(hi), 0), (0, 0, 0.0, 0.0, 1)]], m,
+                          np.zeros(m.shape, np.int32), [1], want_stages=True)[1]
+    assert st[0, 0].tolist() == [3, 1, 3, 2, 3]              # unsure at θ±, strict outward
+    assert st[0, 1].tolist() == [1, 0, 2, 0, 2]              # final θ_f = 0 (0: not reached; tie rejects)
     fin = oracle.run_plans([[(0, 0, 1.25, 1.25, 1)]], m, np.zeros(m.shape, np.int32), [1],
                            want_alive=True)[1]
     assert fin[0].tolist() == [0, 1, 0, 0, 0]                 # only m > θ_f accepted
