@@ -36,7 +36,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5",
+                    help="C5 (default: the largest single-GPU config, 64-plan grid), C2, C3, C4")
+    ap.add_argument("--placement", default="",
+                    help="page placement override (default: the workload's, 'affine' = scattered)")
+    ap.add_argument("--dump-counts", default="",
+                    help="rank 0 writes the final int64 count array (.npy) here (tests)")
     ap.add_argument("--n-tuples", type=int, default=0, help="override tuples per rank")
     ap.add_argument("--impl", default="ko", choices=["ko", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -117,6 +122,18 @@ def algorithmic_bytes(wl, seq_len, n_plans):
     gold = sp.n_ops * n
     out = 8 * sp.n_ops * len(wl.variants) * n
     return kv + meta + gold + out, kv
+
+
+def gold_from_profiling(ko, torch, wl, kv, ops):
+    """uint8 [n_ops][n] gold of every tuple: filters 1 iff the gold variant's margin > 0, maps the
+    gold variant's argmax class (P_g, computed by the product outside the timed region)."""
+    gv = wl.gold_variant
+    m, c, _ = ko.score_batch(kv, ops, [wl.variants[gv]])
+    g = torch.empty((wl.spec.n_ops, kv.n_tuples), dtype=torch.uint8, device=m.device)
+    for o, C in enumerate(wl.spec.op_classes):
+        g[o] = (m[o, 0] > 0).to(torch.uint8) if C <= 1 else c[o, 0].to(torch.uint8)
+    del m, c
+    return g
 
 
 class ClockSampler:
@@ -296,9 +313,14 @@ def main():
         import torch.distributed as dist
         backend = os.environ.get("KO_DIST_BACKEND", "nccl")   # gloo: the same path on one GPU
         if backend == "nccl":
+            # NCCL logs each communicator's rank / nranks at init (visible in the run's stderr)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        print(f"[bench] rank {dist.get_rank()} of {dist.get_world_size()}: process group "
+              f"backend {dist.get_backend()}, cuda:{local}", file=sys.stderr, flush=True)
 
     wl = workloads.get(args.config)
     n_per = args.n_tuples or wl.bench_n or wl.n_tuples
@@ -306,10 +328,15 @@ def main():
     # .. r·n_per + n_per − 1, or for variable lengths the range balanced by algorithmic bytes
     # (full-read upper bound per tuple)
     t0, n = rank_range(wl, n_per, rank, world)
-    d = device_workload(wl, t0=t0, n=n, placement="contiguous")
-    kv, ops, gold = d["kv"], d["ops"], d["gold"]
+    placement = args.placement or wl.placement
+    d = device_workload(wl, t0=t0, n=n, placement=placement)
+    kv, ops = d["kv"], d["ops"]
     n_var, n_ops = len(wl.variants), wl.spec.n_ops
     plans = wl.plans
+    # labels = the paper's P_g ("the gold pipeline uses only the most expensive operator",
+    # P:763-764 precision/recall against P_g): each op's final decision (θ_f = 0) on its gold
+    # variant, from one profiling pass before the timed region (the labelled sample's labels)
+    gold = gold_from_profiling(ko, torch, wl, kv, ops)
     margins = torch.empty((n_ops, n_var, n), dtype=torch.float32, device="cuda")
     classes = torch.empty((n_ops, n_var, n), dtype=torch.int32, device="cuda")
     counts = torch.zeros((len(plans), ko.COUNTS_PER_PLAN), dtype=torch.int64, device="cuda")
@@ -397,7 +424,9 @@ def main():
                                 if routed else
                                 "grid (all ops x variants in one read + per-tuple plan grid)"),
                        "n_plans": len(plans), "variants": wl.variants,
-                       "kv_bytes_per_rank": kv_bytes,
+                       "kv_bytes_per_rank": kv_bytes, "placement": placement,
+                       "gold": "P_g: each op's gold-variant decision (P:346, P:763-764), from a "
+                               "profiling pass before the timed region",
                        "l2": "inputs larger than L2 (KV per rank >> 126 MB); no flush",
                        "parallelism": f"dp{world} (tuple shards, NCCL all-reduce of counts)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -414,6 +443,8 @@ def main():
             "plan_selection": selection,
         }
         print(json.dumps(line), flush=True)
+        if args.dump_counts:
+            np.save(args.dump_counts, cnt)
     if dist is not None:
         dist.destroy_process_group()
 
@@ -578,7 +609,19 @@ def run_e2e(args, ko, torch, wl, d, ops, gold, plans, margins, classes, counts, 
                                 pin_memory=True)
     except RuntimeError as e:  # noqa: BLE001
         return {"value": None, "unit": UNIT, "error": f"pinned host alloc failed: {e}"[:200]}
-    host_pool.copy_(kv.pool[:n_pages])     # fill the host copy (outside the timed region)
+    # The host holds the batch's pages in logical (tuple-major) order, the natural layout of a
+    # store streamed from host memory; the e2e view uses the matching contiguous page table, so a
+    # tuple chunk is one contiguous page range (filled outside the timed region).
+    ids_dev = kv.page_ids.to(torch.int64)
+    step_p = max(1, (4 << 30) // page_bytes)
+    for a in range(0, n_pages, step_p):
+        b = min(n_pages, a + step_p)
+        host_pool[a:b].copy_(kv.pool.index_select(0, ids_dev[a:b]))
+    torch.cuda.synchronize()
+    kv = ko.KVCache(pool=kv.pool, page_indptr=kv.page_indptr,
+                    page_ids=torch.arange(kv.page_ids.numel(), dtype=torch.int32, device="cuda"),
+                    seq_len=kv.seq_len, n_layers=kv.n_layers, n_kv_heads=kv.n_kv_heads,
+                    gqa_group=kv.gqa_group, head_dim=kv.head_dim, n_q=kv.n_q)
     h_margins = torch.empty(margins.shape, dtype=margins.dtype, pin_memory=True)
     h_counts = torch.empty(counts.shape, dtype=counts.dtype, pin_memory=True)
     n_chunks = 8

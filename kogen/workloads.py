@@ -32,6 +32,7 @@ class Workload:
     mode: str = "grid"                         # "grid" (profiling + plan grid) or "routed"
     bias: Optional[List[List[float]]] = None   # [op][class]
     bench_n: int = 0                           # tuples per rank per bench step (resident batch)
+    placement: str = "affine"                  # bench page placement: scattered pages (page_table)
 
     def biases(self) -> List[List[float]]:
         if self.bias is not None:
