@@ -403,12 +403,21 @@ def main():
     # host derivation (row a12 / NEXT-2): cheapest plan of the grid meeting the recall target
     selection = None
     if rank == 0 and len(plans) > 1:
+        # NEXT-2 on the pass's counts: cheapest plan meeting ℓ_α^R ≥ 0.9 (labels = P_g), its
+        # loss L (eqn:loss, β = 10) and Target Met = achieved recall / target
         from paper_2602_04430_b200 import plan_select
-        best, _ = plan_select.select_plan(plans, cnt, wl.variants, target_recall=0.9)
-        selection = {"target_recall": 0.9, "alpha": 0.95,
+        best, _ = plan_select.select_plan(plans, cnt, wl.variants, target_recall=0.9,
+                                          n_tuples=world * n_per)
+        selection = {"target_recall": 0.9, "alpha": 0.95, "beta": 10.0,
+                     "labels": "P_g (gold-variant decisions)",
                      "plan": None if best is None else best.index,
                      "cost_vs_gold": None if best is None else best.cost / (world * n_per * wl.spec.n_ops),
-                     "recall_lb": None if best is None else best.recall_lb}
+                     "recall_lb": None if best is None else best.recall_lb,
+                     "recall": None if best is None else best.recall,
+                     "precision": None if best is None else best.precision,
+                     "target_met_recall": None if best is None else best.loss["target_met_recall"],
+                     "loss": None if best is None else best.loss["loss"],
+                     "l_cost": None if best is None else best.loss["l_cost"]}
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

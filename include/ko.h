@@ -247,6 +247,39 @@ size_t ko_workspace_size(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
  * Returns NaN on invalid input (a < 0, b < 0, alpha outside (0,1)).                           */
 double ko_beta_lower_bound(int64_t a, int64_t b, double alpha);
 
+/* Host helper: ko_beta_lower_bound for real-valued (soft, relaxed) counts a, b >= 0 — the bound
+ * the gradient loop differentiates — and its partial derivatives dℓ/da, dℓ/db (either
+ * pointer may be NULL) by implicit differentiation of I_ℓ(1+a, 1+b) = 1 − α:
+ * dℓ/da = −(∂I/∂a)/(∂I/∂x), ∂I/∂x the Beta density, ∂I/∂a central differences of I.
+ * Returns NaN on invalid input. */
+double ko_beta_lower_bound_real(double a, double b, double alpha, double* dl_da, double* dl_db);
+
+/* Loss of the operator-selection objective (eqn:cost-loss … eqn:loss; NEXT-2):
+ *   L_cost = cost / (|S| · Σ_i cost_{o_i}),   L_R = ReLU(T_R − ℓ_α^R),   L_P = ReLU(T_P − ℓ_α^P),
+ *   L = L_cost + β·L_P + β·L_R,
+ * ℓ_α^R = I^{-1}(1 − α; 1 + TP, 1 + FN), ℓ_α^P = I^{-1}(1 − α; 1 + TP, 1 + FP) (Eqs. 8–9, real
+ * counts).  "The loss on precision and recall are only active (gradient ≠ 0) if the current
+ * pipeline violates the respective target": at T = ℓ the constraint term contributes 0.
+ * stats: HOST double [4] = {TP, FP, FN, cost} — hard counts (cost = Σ_s n_in[s]·stage_cost[s]) or
+ *        ko_soft_stats' first four outputs (soft counts, σ-scaled cost).
+ * jacobian: HOST double [4][n_params] = d{TP, FP, FN, cost}/d params (ko_soft_stats' layout, at
+ *        out + 4 with n_params = 3·n_stages), or NULL with n_params = 0.
+ * n_tuples: |S|; stage_cost: HOST double [n_stages] = cost_{o_i} of the plan's stages.
+ * out: HOST double [10] = {L, L_cost, L_R, L_P, ℓ_R, ℓ_P, recall, precision, Target Met recall,
+ *        Target Met precision}; Target Met = achieved / target (NaN for a zero target),
+ *        achieved = TP/(TP+FN) and TP/(TP+FP) (1 when the denominator is 0, Q20).
+ * grad: HOST double [n_params] = dL/d params by the chain rule through ℓ, or NULL.
+ * Errors: KO_EINVAL (NULL/negative/NaN inputs, alpha outside (0,1), β < 0).  Host only.       */
+typedef struct {
+  double target_recall;    /* T_R (0 = no recall constraint)                                 */
+  double target_precision; /* T_P (0 = no precision constraint)                              */
+  double alpha;            /* credible level α of the lower bounds               */
+  double beta;             /* constraint weight β of eqn:loss                                */
+} ko_loss_params;
+ko_status ko_plan_loss(const double* stats, const double* jacobian, int32_t n_params,
+                       double n_tuples, const double* stage_cost, int32_t n_stages,
+                       const ko_loss_params* lp, double* out, double* grad);
+
 /* Tracing hook (runtime profiling): when ev_begin/ev_end (cudaEvent_t handles) are non-NULL,
  * every later ko_score_batch call on this thread records ev_begin on its stream immediately before
  * its first scoring-kernel launch and ev_end immediately after its last one, so a caller can time

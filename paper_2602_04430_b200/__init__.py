@@ -58,6 +58,11 @@ class _Plan(ctypes.Structure):
     _fields_ = [("n_stages", ctypes.c_int32), ("stage", _Stage * MAX_STAGES)]
 
 
+class _LossParams(ctypes.Structure):
+    _fields_ = [("target_recall", ctypes.c_double), ("target_precision", ctypes.c_double),
+                ("alpha", ctypes.c_double), ("beta", ctypes.c_double)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py` "
@@ -84,6 +89,11 @@ def _load():
     L.ko_soft_stats.restype = ctypes.c_int
     L.ko_soft_workspace_size.argtypes = [I32, I64]
     L.ko_soft_workspace_size.restype = ctypes.c_size_t
+    L.ko_beta_lower_bound_real.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, P, P]
+    L.ko_beta_lower_bound_real.restype = ctypes.c_double
+    L.ko_plan_loss.argtypes = [P, P, I32, ctypes.c_double, P, I32, ctypes.POINTER(_LossParams),
+                               P, P]
+    L.ko_plan_loss.restype = ctypes.c_int
     L.ko_set_trace_events.argtypes = [P, P]
     L.ko_set_trace_events.restype = None
     L.ko_last_error.restype = ctypes.c_char_p
@@ -94,7 +104,8 @@ def _load():
 
 _lib = _load()
 EXPORTS = ("ko_score_batch", "ko_route", "ko_reduce_stats", "ko_workspace_size",
-           "ko_embed_scores", "ko_build_importance_order", "ko_soft_stats", "ko_soft_workspace_size", "ko_beta_lower_bound",
+           "ko_embed_scores", "ko_build_importance_order", "ko_soft_stats", "ko_soft_workspace_size",
+           "ko_beta_lower_bound", "ko_beta_lower_bound_real", "ko_plan_loss",
            "ko_set_trace_events", "ko_last_error", "ko_version", "ko_last_launch_count")
 
 
@@ -349,3 +360,36 @@ def beta_lower_bound(a: int, b: int, alpha: float) -> float:
 def abi_ok() -> bool:
     """True when every symbol include/ko.h declares is exported by the loaded library."""
     return all(hasattr(_lib, s) for s in EXPORTS)
+
+
+def beta_lower_bound_real(a: float, b: float, alpha: float):
+    """ko_beta_lower_bound_real: (ℓ, dℓ/da, dℓ/db) for real-valued counts."""
+    da, db = ctypes.c_double(), ctypes.c_double()
+    v = float(_lib.ko_beta_lower_bound_real(float(a), float(b), float(alpha), ctypes.byref(da),
+                                            ctypes.byref(db)))
+    return v, da.value, db.value
+
+
+LOSS_FIELDS = ("loss", "l_cost", "l_recall", "l_precision", "recall_lb", "precision_lb", "recall",
+               "precision", "target_met_recall", "target_met_precision")
+
+
+def plan_loss(stats: Sequence[float], stage_cost: Sequence[float], n_tuples: float,
+              target_recall: float = 0.0, target_precision: float = 0.0, alpha: float = 0.95,
+              beta: float = 10.0, jacobian=None):
+    """ko_plan_loss (host).  stats = (TP, FP, FN, cost); jacobian: None or a [4][n_params] array
+    (e.g. ko_soft_stats' out[4:].reshape(4, -1)).  Returns (dict of LOSS_FIELDS, grad list)."""
+    import numpy as np
+    st = (ctypes.c_double * 4)(*[float(x) for x in stats[:4]])
+    sc = (ctypes.c_double * len(stage_cost))(*[float(x) for x in stage_cost])
+    n_par, jac, grad = 0, None, None
+    if jacobian is not None:
+        J = np.ascontiguousarray(np.asarray(jacobian, np.float64).reshape(4, -1))
+        n_par = J.shape[1]
+        jac = (ctypes.c_double * J.size)(*J.ravel().tolist())
+        grad = (ctypes.c_double * max(n_par, 1))()
+    out = (ctypes.c_double * 10)()
+    lp = _LossParams(float(target_recall), float(target_precision), float(alpha), float(beta))
+    _check(_lib.ko_plan_loss(st, jac, n_par, float(n_tuples), sc, len(stage_cost),
+                             ctypes.byref(lp), out, grad))
+    return dict(zip(LOSS_FIELDS, list(out))), (list(grad)[:n_par] if grad is not None else None)

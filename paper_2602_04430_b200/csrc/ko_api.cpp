@@ -964,15 +964,109 @@ static double betainc_reg(double a, double b, double x) {
   return 1.0 - std::exp(lbt) * betacf(b, a, 1.0 - x) / b;
 }
 
-double ko_beta_lower_bound(int64_t a_cnt, int64_t b_cnt, double alpha) {
-  if (a_cnt < 0 || b_cnt < 0 || !(alpha > 0.0 && alpha < 1.0)) return NAN;
-  const double a = 1.0 + (double)a_cnt, b = 1.0 + (double)b_cnt, target = 1.0 - alpha;
+// x with I_x(a, b) = p (a, b > 0 real) by bisection: I is increasing in x.
+static double betainc_inv(double a, double b, double p) {
   double lo = 0.0, hi = 1.0;
   for (int it = 0; it < 200 && hi - lo > 1e-16; ++it) {
     const double mid = 0.5 * (lo + hi);
-    if (betainc_reg(a, b, mid) < target) lo = mid; else hi = mid;
+    if (betainc_reg(a, b, mid) < p) lo = mid; else hi = mid;
   }
   return 0.5 * (lo + hi);
+}
+
+double ko_beta_lower_bound(int64_t a_cnt, int64_t b_cnt, double alpha) {
+  if (a_cnt < 0 || b_cnt < 0 || !(alpha > 0.0 && alpha < 1.0)) return NAN;
+  return betainc_inv(1.0 + (double)a_cnt, 1.0 + (double)b_cnt, 1.0 - alpha);
+}
+
+double ko_beta_lower_bound_real(double a_cnt, double b_cnt, double alpha, double* dl_da,
+                                double* dl_db) {
+  if (!(a_cnt >= 0.0) || !(b_cnt >= 0.0) || !std::isfinite(a_cnt) || !std::isfinite(b_cnt) ||
+      !(alpha > 0.0 && alpha < 1.0))
+    return NAN;
+  const double A = 1.0 + a_cnt, B = 1.0 + b_cnt, p = 1.0 - alpha;
+  const double x = betainc_inv(A, B, p);
+  // Implicit differentiation of I_x(A, B) = p: dx/dA = −(∂I/∂A)/(∂I/∂x), with
+  // ∂I/∂x the Beta(A, B) density at x and ∂I/∂A, ∂I/∂B central differences of I in the shape
+  // (step 1e-5·max(1, shape)).  dA/da = dB/db = 1.
+  if (dl_da || dl_db) {
+    double da = 0.0, db = 0.0;
+    if (x > 0.0 && x < 1.0) {
+      const double log_dens = (A - 1.0) * std::log(x) + (B - 1.0) * std::log1p(-x) -
+                              (std::lgamma(A) + std::lgamma(B) - std::lgamma(A + B));
+      const double dens = std::exp(log_dens);
+      if (dens > 0.0) {
+        const double ha = 1e-5 * std::max(1.0, A), hb = 1e-5 * std::max(1.0, B);
+        const double dIdA = (betainc_reg(A + ha, B, x) - betainc_reg(A - ha, B, x)) / (2.0 * ha);
+        const double dIdB = (betainc_reg(A, B + hb, x) - betainc_reg(A, B - hb, x)) / (2.0 * hb);
+        da = -dIdA / dens;
+        db = -dIdB / dens;
+      }
+    }
+    if (dl_da) *dl_da = da;
+    if (dl_db) *dl_db = db;
+  }
+  return x;
+}
+
+ko_status ko_plan_loss(const double* stats, const double* jacobian, int32_t n_params,
+                       double n_tuples, const double* stage_cost, int32_t n_stages,
+                       const ko_loss_params* lp, double* out, double* grad) {
+  g_launches = 0;
+  if (!stats || !stage_cost || !lp || !out) return fail(KO_EINVAL, "ko_plan_loss: NULL argument");
+  if (n_params < 0 || (n_params > 0 && !jacobian) || (grad && n_params > 0 && !jacobian))
+    return fail(KO_EINVAL, "ko_plan_loss: n_params %d without a jacobian", n_params);
+  if (n_stages < 1 || n_stages > KO_MAX_STAGES) return fail(KO_EINVAL, "n_stages %d", n_stages);
+  if (!(n_tuples > 0.0)) return fail(KO_EINVAL, "n_tuples must be > 0");
+  if (!(lp->alpha > 0.0 && lp->alpha < 1.0)) return fail(KO_EINVAL, "alpha outside (0,1)");
+  if (!(lp->beta >= 0.0) || !std::isfinite(lp->beta)) return fail(KO_EINVAL, "beta must be >= 0");
+  const double tp = stats[0], fp = stats[1], fn = stats[2], cost = stats[3];
+  if (!(tp >= 0.0 && fp >= 0.0 && fn >= 0.0 && cost >= 0.0))
+    return fail(KO_EINVAL, "ko_plan_loss: negative or NaN TP/FP/FN/cost");
+  double csum = 0.0;  // Σ_i cost_{o_i} over the plan's stages (eqn:cost-loss)
+  for (int i = 0; i < n_stages; ++i) {
+    if (!(stage_cost[i] >= 0.0) || !std::isfinite(stage_cost[i]))
+      return fail(KO_EINVAL, "stage_cost[%d] negative or non-finite", i);
+    csum += stage_cost[i];
+  }
+  if (!(csum > 0.0)) return fail(KO_EINVAL, "sum of stage costs must be > 0");
+  const double norm = n_tuples * csum;
+  double dR_dtp, dR_dfn, dP_dtp, dP_dfp;
+  const double lR = ko_beta_lower_bound_real(tp, fn, lp->alpha, &dR_dtp, &dR_dfn);
+  const double lP = ko_beta_lower_bound_real(tp, fp, lp->alpha, &dP_dtp, &dP_dfp);
+  const double L_cost = cost / norm;
+  const double L_R = std::max(0.0, lp->target_recall - lR);
+  const double L_P = std::max(0.0, lp->target_precision - lP);
+  const bool act_R = lp->target_recall > lR, act_P = lp->target_precision > lP;
+  out[0] = L_cost + lp->beta * L_P + lp->beta * L_R;
+  out[1] = L_cost;
+  out[2] = L_R;
+  out[3] = L_P;
+  out[4] = lR;
+  out[5] = lP;
+  // Target Met: achieved / target, achieved = the point recall / precision of the counts
+  // (an empty output has precision 1, Q20); NaN for a zero target
+  const double rec = tp + fn > 0.0 ? tp / (tp + fn) : 1.0;
+  const double prec = tp + fp > 0.0 ? tp / (tp + fp) : 1.0;
+  out[6] = rec;
+  out[7] = prec;
+  out[8] = lp->target_recall > 0.0 ? rec / lp->target_recall : NAN;
+  out[9] = lp->target_precision > 0.0 ? prec / lp->target_precision : NAN;
+  if (grad) {
+    // dL/dp = (dcost/dp)/norm − β·[T_R > ℓ_R]·dℓ_R/dp − β·[T_P > ℓ_P]·dℓ_P/dp; the Jacobian rows
+    // are (TP, FP, FN, cost) × n_params (ko_soft_stats' layout)
+    const double* J_tp = jacobian;
+    const double* J_fp = jacobian + n_params;
+    const double* J_fn = jacobian + 2 * (size_t)n_params;
+    const double* J_c = jacobian + 3 * (size_t)n_params;
+    for (int k = 0; k < n_params; ++k) {
+      double g = J_c[k] / norm;
+      if (act_R) g -= lp->beta * (dR_dtp * J_tp[k] + dR_dfn * J_fn[k]);
+      if (act_P) g -= lp->beta * (dP_dtp * J_tp[k] + dP_dfp * J_fp[k]);
+      grad[k] = g;
+    }
+  }
+  return KO_OK;
 }
 
 }  // extern "C"

@@ -49,3 +49,27 @@ def test_infeasible_returns_none():
     counts[0, 5] = 100
     best, _ = plan_select.select_plan([[(0, 0, 0.0, 0.0, 1)]], counts, [(1000, 1)], 0.9)
     assert best is None
+
+
+def test_selection_carries_loss_and_target_met():
+    """Every plan's loss (eqn:loss) and Target Met on its hard counts equal the loss
+    oracle's, with cost = Σ_s n_in[s]·cost_s and Σ_i cost_{o_i} over the plan's stages."""
+    from oracle import loss
+    rng = np.random.default_rng(9)
+    n = 3000
+    m = rng.normal(0, 2, size=(2, 3, n))
+    gold = ((m[:, 2] + rng.normal(0, 0.3, size=(2, n))) > 0).astype(np.uint8)
+    variants = [(200, 1), (500, 2), (1000, 2)]
+    plans = [[(0, 0, -h, h, 0), (0, 2, 0.0, 0.0, 1), (1, 1, -h, h, 0), (1, 2, 0.0, 0.0, 1)]
+             for h in (0.25, 1.0, 3.0)]
+    counts = oracle.run_plans(plans, m, np.zeros(m.shape, np.int32), [1, 1], gold)
+    best, stats = plan_select.select_plan(plans, counts, variants, target_recall=0.9,
+                                          target_precision=0.8, n_tuples=n)
+    vc = plan_select.variant_costs(variants)
+    for st, pl, c in zip(stats, plans, counts):
+        sc = [vc[s[1]] for s in pl]
+        cost = sum(c[5 + 4 * k] * sc[k] for k in range(len(pl)))
+        exp = loss.loss(c[0], c[1], c[2], cost, n, sc, 0.9, 0.8, 0.95, 10.0)
+        for k, v in exp.items():
+            assert abs(st.loss[k] - v) <= 1e-10 * max(1.0, abs(v)), k
+        assert abs(st.loss["target_met_recall"] - st.recall / 0.9) < 1e-12

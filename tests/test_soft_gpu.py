@@ -6,7 +6,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from oracle import soft  # noqa: E402
+from oracle import loss, soft  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -46,3 +46,22 @@ def test_soft_stats_rejects_maps(ko):
     m = torch.zeros((1, 1, 4), device="cuda")
     with pytest.raises(ko.KoError, match="map"):
         ko.soft_stats([(0, 0, 0.0, 0.0, 1)], [0.0], [1.0], 1.0, m, [3])
+
+
+@pytest.mark.parametrize("tr,tpr", [(0.05, 0.05), (0.99, 0.99)])
+def test_loss_gradient_through_gpu_jacobian(ko, tr, tpr):
+    """NEXT-2 chain: ko_soft_stats' GPU Jacobian → ko_plan_loss → dL/d(s, θ⁻, θ⁺), against the
+    oracle's relaxation + loss (oracle/loss.py)."""
+    rng = np.random.default_rng(17)
+    n = 20000
+    m = rng.normal(0, 2, size=(2, 2, n)).astype(np.float32)
+    gold = (rng.random((2, n)) < 0.4).astype(np.uint8)
+    plan = [(0, 0, -0.8, 0.6, 0), (0, 1, 0.0, 0.0, 1), (1, 0, -0.4, 0.9, 0), (1, 1, 0.1, 0.1, 1)]
+    pick, cost = [0.2, 0.0, -0.1, 0.0], [0.25, 1.0, 0.3, 1.0]
+    vals_or, grad_or, _ = loss.soft_loss(plan, pick, 0.3, m.astype(np.float64), gold, cost, tr,
+                                         tpr, 0.95, 10.0)
+    out = ko.soft_stats(plan, pick, cost, 0.3, torch.from_numpy(m).cuda(), [1, 1],
+                        gold=torch.from_numpy(gold).cuda()).cpu().numpy()
+    v, g = ko.plan_loss(out[:4], cost, n, tr, tpr, 0.95, 10.0, jacobian=out[4:].reshape(4, -1))
+    assert abs(v["loss"] - vals_or["loss"]) <= 1e-9 * max(1.0, vals_or["loss"])
+    assert np.allclose(g, grad_or, rtol=1e-6, atol=1e-9 * np.abs(grad_or).max())
