@@ -314,8 +314,8 @@ def main():
         backend = os.environ.get("KO_DIST_BACKEND", "nccl")   # gloo: the same path on one GPU
         if backend == "nccl":
             # NCCL logs each communicator's rank / nranks at init (visible in the run's stderr)
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ["NCCL_DEBUG"] = os.environ.get("KO_NCCL_DEBUG", "INFO")
+            os.environ["NCCL_DEBUG_SUBSYS"] = os.environ.get("KO_NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)

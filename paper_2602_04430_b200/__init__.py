@@ -157,8 +157,8 @@ class KVCache:
             if not t.is_cuda:
                 raise ValueError(f"KVCache.{name} must be a CUDA tensor (no CPU path)")
         return _KV(self.n_layers, self.n_kv_heads, self.gqa_group, self.head_dim, self.n_q,
-                   self.pool.data_ptr(), int(self.pool.shape[0]), self.page_indptr.data_ptr(),
-                   self.page_ids.data_ptr(), self.seq_len.data_ptr(), self.n_tuples)
+                   _dp(self.pool), int(self.pool.shape[0]), _dp(self.page_indptr),
+                   _dp(self.page_ids), _dp(self.seq_len), self.n_tuples)
 
 
 @dataclass
@@ -183,7 +183,7 @@ def _ops(ops: Sequence[Operator]):
         w_bf16 = 1 if o.w.dtype == torch.bfloat16 else 0
         if not w_bf16 and o.w.dtype != torch.float32:
             raise ValueError("Operator.w must be float32 or bfloat16")
-        arr[i] = _Op(int(o.n_classes), o.q.data_ptr(), o.w.data_ptr(), o.b.data_ptr(), w_bf16)
+        arr[i] = _Op(int(o.n_classes), _dp(o.q), _dp(o.w), _dp(o.b), w_bf16)
     return arr
 
 
@@ -202,8 +202,18 @@ def make_plans(plans: Sequence[Sequence[Stage]]):
     return arr
 
 
+def _dp(t) -> int:
+    """Device pointer of a dense CUDA tensor.  The C ABI takes plain pointers to row-major arrays,
+    so a strided view would be read with the wrong layout: refuse it (and host tensors)."""
+    if not t.is_cuda:
+        raise ValueError("tensor arguments must be CUDA tensors (there is no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"tensor of shape {tuple(t.shape)} is not contiguous: pass .contiguous()")
+    return t.data_ptr()
+
+
 def _ptr(t) -> Optional[int]:
-    return None if t is None else t.data_ptr()
+    return None if t is None else _dp(t)
 
 
 def _stream(stream) -> Optional[int]:
@@ -254,7 +264,7 @@ def score_batch(kv: KVCache, ops: Sequence[Operator], variants: Sequence[Tuple[i
     rc = _lib.ko_score_batch(ctypes.byref(kv._c()), _ops(ops), n_ops, _variants(variants), n_var,
                              _ptr(tuple_idx), n_work if tuple_idx is not None else 0,
                              _ptr(margins), _ptr(classes), parr, n_plans, _ptr(gold),
-                             _ptr(counts), workspace.data_ptr(), workspace.numel(),
+                             _ptr(counts), _dp(workspace), workspace.numel(),
                              _stream(stream))
     _check(rc)
     return margins, classes, counts
@@ -268,9 +278,9 @@ def route(plan: Sequence[Stage], margins, classes, n_classes: Sequence[int], sta
     if counts is None:
         counts = torch.zeros((1, COUNTS_PER_PLAN), dtype=torch.int64, device=margins.device)
     nc = (ctypes.c_int32 * n_ops)(*[int(c) for c in n_classes])
-    rc = _lib.ko_route(make_plans([plan]), margins.data_ptr(), _ptr(classes), nc, n_ops, n_var, n,
-                       stage, tuple_state.data_ptr(), _ptr(worklist), _ptr(worklist_len),
-                       _ptr(gold), counts.data_ptr(), _stream(stream))
+    rc = _lib.ko_route(make_plans([plan]), _dp(margins), _ptr(classes), nc, n_ops, n_var, n,
+                       stage, _dp(tuple_state), _ptr(worklist), _ptr(worklist_len),
+                       _ptr(gold), _dp(counts), _stream(stream))
     _check(rc)
     return counts
 
@@ -284,8 +294,8 @@ def reduce_stats(plans: Sequence[Sequence[Stage]], margins, classes, n_classes: 
         counts = torch.zeros((len(plans), COUNTS_PER_PLAN), dtype=torch.int64,
                              device=margins.device)
     nc = (ctypes.c_int32 * n_ops)(*[int(c) for c in n_classes])
-    rc = _lib.ko_reduce_stats(make_plans(plans), len(plans), margins.data_ptr(), _ptr(classes),
-                              nc, n_ops, n_var, n, _ptr(gold), counts.data_ptr(), _stream(stream))
+    rc = _lib.ko_reduce_stats(make_plans(plans), len(plans), _dp(margins), _ptr(classes),
+                              nc, n_ops, n_var, n, _ptr(gold), _dp(counts), _stream(stream))
     _check(rc)
     return counts
 
@@ -293,8 +303,8 @@ def reduce_stats(plans: Sequence[Sequence[Stage]], margins, classes, n_classes: 
 def build_importance_order(src: KVCache, mu, sigma2, dst_pool, dst_page_ids, stream=None):
     """ko_build_importance_order: dst_pool (same geometry, pages dst_page_ids under the same
     CSR) receives every tuple's tokens in descending expected-attention order."""
-    rc = _lib.ko_build_importance_order(ctypes.byref(src._c()), mu.data_ptr(), sigma2.data_ptr(),
-                                        dst_pool.data_ptr(), dst_page_ids.data_ptr(),
+    rc = _lib.ko_build_importance_order(ctypes.byref(src._c()), _dp(mu), _dp(sigma2),
+                                        _dp(dst_pool), _dp(dst_page_ids),
                                         _stream(stream))
     _check(rc)
     return dst_pool
@@ -309,9 +319,9 @@ def embed_scores(item_emb, op_emb, op_ids: Sequence[int], margins, variant: int,
     n_ops, n_var, n = margins.shape
     ids = (ctypes.c_int32 * len(op_ids))(*[int(x) for x in op_ids])
     n_idx = 0 if tuple_idx is None else int(tuple_idx.numel())
-    rc = _lib.ko_embed_scores(item_emb.data_ptr(), int(item_emb.shape[1]), int(item_emb.shape[0]),
-                              op_emb.data_ptr(), int(op_emb.shape[0]), ids, n_ops, int(variant),
-                              n_var, _ptr(tuple_idx), n_idx, margins.data_ptr(), _stream(stream))
+    rc = _lib.ko_embed_scores(_dp(item_emb), int(item_emb.shape[1]), int(item_emb.shape[0]),
+                              _dp(op_emb), int(op_emb.shape[0]), ids, n_ops, int(variant),
+                              n_var, _ptr(tuple_idx), n_idx, _dp(margins), _stream(stream))
     _check(rc)
     return margins
 
@@ -332,8 +342,8 @@ def soft_stats(plan: Sequence[Stage], pick_scores: Sequence[float], stage_cost: 
     pk = (ctypes.c_double * S)(*[float(x) for x in pick_scores])
     cs = (ctypes.c_double * S)(*[float(x) for x in stage_cost])
     nc = (ctypes.c_int32 * n_ops)(*[int(c) for c in n_classes])
-    rc = _lib.ko_soft_stats(make_plans([plan]), pk, cs, float(tau), margins.data_ptr(), nc, n_ops,
-                            n_var, n, _ptr(gold), out.data_ptr(), workspace.data_ptr(),
+    rc = _lib.ko_soft_stats(make_plans([plan]), pk, cs, float(tau), _dp(margins), nc, n_ops,
+                            n_var, n, _ptr(gold), _dp(out), _dp(workspace),
                             workspace.numel(), _stream(stream))
     _check(rc)
     return out

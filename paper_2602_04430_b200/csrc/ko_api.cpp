@@ -310,6 +310,7 @@ void fill_common(ko::ScoreParams& sp, ko::PrepParams& pp, const ko_kv_cache* kv,
   sp.page_ids = kv->page_ids;
   sp.seq_len = kv->seq_len;
   sp.n_tuples = kv->n_tuples;
+  sp.n_pages = kv->n_pages;
   sp.n_layers = kv->n_layers;
   sp.n_kv_heads = kv->n_kv_heads;
   sp.gqa = kv->gqa_group;
@@ -870,6 +871,7 @@ ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, con
   bp.dst_ids = dst_page_ids;
   bp.inv_sqrt_d = 1.0 / std::sqrt((double)src->head_dim);
   bp.inv_2d = 1.0 / (2.0 * (double)src->head_dim);
+  bp.n_pages = src->n_pages;
   KO_LAUNCH(ko::launch_build(bp, (cudaStream_t)stream));
   ++g_launches;  // launch_build: two kernels (short / long tuples)
   return KO_OK;

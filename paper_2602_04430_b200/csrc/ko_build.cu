@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
     const int64_t t = u / (Lyr * H);
     const int l = (int)((u / H) % Lyr), h = (int)(u % H);
     const int L = p.seq_len[t];
+    KO_DCHECK(L >= 1);
     if (L <= MINT || L > MAXT) continue;  // the other launch's (or > 4096: documented, skipped)
     __syncthreads();
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
     const int off_k = ((l * 2 + 0) * H + h) * 16 * D, off_v = ((l * 2 + 1) * H + h) * 16 * D;
     auto src_row = [&](int which, int i) -> const uint16_t* {
       const int64_t page = p.src_ids[pbase + (i >> 4)];
+      KO_DCHECK(page >= 0 && page < p.n_pages);
       return p.src_pool + (size_t)page * p.page_elems + (which ? off_v : off_k) + (i & 15) * D;
     };
     int N = 64;  // ≥ one warp segment (padding sorts last)

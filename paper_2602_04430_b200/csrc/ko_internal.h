@@ -9,6 +9,25 @@
 
 #include "ko.h"
 
+// Device-side checks of caller data (ko.h: "device-data errors are undefined behaviour" in the
+// release build).  The KO_DEBUG build (lib/libko_debug.so, same ABI) traps on a page id outside
+// [0, n_pages), seq_len < 1 or a tuple id outside [0, n_tuples), after printing the failed check.
+#ifdef KO_DEBUG
+#include <cstdio>
+#define KO_DCHECK(cond)                                                                       \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("KO_DEBUG check failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,    \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                    \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define KO_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace ko {
 
 constexpr int kMaxOps = KO_MAX_OPS;
@@ -34,6 +53,7 @@ struct ScoreParams {
   const int32_t* page_ids;
   const int32_t* seq_len;
   int64_t n_tuples;
+  int64_t n_pages;  // pool pages (KO_DEBUG bounds check of page ids)
   int32_t n_layers, n_kv_heads, gqa, n_q;
   // work list (tuple ids); NULL = identity.  Length from work_len_dev if non-NULL.
   const int32_t* work;
@@ -180,6 +200,7 @@ struct BuildParams {
   uint16_t* dst_pool;
   const int32_t* dst_ids;
   double inv_sqrt_d, inv_2d;
+  int64_t n_pages;  // pages of src and dst pools (KO_DEBUG bounds checks)
 };
 cudaError_t launch_build(const BuildParams& p, cudaStream_t s);
 

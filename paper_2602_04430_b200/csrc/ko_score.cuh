@@ -212,7 +212,9 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     U.l = unit / (Hkv / HG);
     U.h0 = (unit - U.l * (Hkv / HG)) * HG;
     U.t = p.work ? (int64_t)p.work[U.wslot] : U.wslot;
+    KO_DCHECK(U.t >= 0 && U.t < p.n_tuples);
     U.L = p.seq_len[U.t];
+    KO_DCHECK(U.L >= 1);
     U.pbase = p.page_indptr[U.t];
     // tokens [s0, s1): s1 = the largest prefix among the streamed variants whose cut includes l;
     // walk mode resumes after the extent of the tuple's previous rank for this group (s0)
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     U.pid_chunk = U.ipg >> 5;
     const int idx = (U.pid_chunk << 5) + lane;
     if (idx < ((U.s1 + 15) >> 4)) U.pid_reg = __ldg(p.page_ids + U.pbase + idx);
+    KO_DCHECK(U.pid_reg >= 0 && U.pid_reg < p.n_pages);
     return U;
   };
   auto n_pages_of = [&](const Unit& U) {  // pages streamed per kv-head
@@ -244,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     if (chunk != U.pid_chunk) {
       const int idx = (chunk << 5) + lane;
       U.pid_reg = idx < pg1u ? __ldg(p.page_ids + U.pbase + idx) : 0;
+      KO_DCHECK(U.pid_reg >= 0 && U.pid_reg < p.n_pages);
       U.pid_chunk = chunk;
     }
     const int pid = __shfl_sync(0xffffffffu, U.pid_reg, pg & 31);

@@ -98,3 +98,11 @@ def test_beta_lower_bound_host_helper():
     for a, b in [(19, 1), (90, 10), (900, 100), (9000, 800), (45000, 3000), (3, 77)]:
         assert abs(ko.beta_lower_bound(a, b, 0.95) - oracle.beta_lower_bound(a, b, 0.95)) < 1e-10
     assert math.isnan(ko.beta_lower_bound(-1, 0, 0.95))
+
+
+def test_binding_refuses_host_tensors():
+    """No CPU path: the binding hands the C ABI device pointers only (and dense arrays only)."""
+    import torch
+    import paper_2602_04430_b200 as ko
+    with pytest.raises(ValueError, match="CUDA"):
+        ko._dp(torch.zeros(4))

@@ -15,6 +15,7 @@ The oracle reads the generator's pages copied from the device (tests/fullsize.py
 against the host twin)."""
 import gc
 import time
+import traceback
 
 import numpy as np
 import pytest
@@ -71,53 +72,65 @@ def test_full_size_vs_oracle(ko, name):
     n = wl.bench_n
     routed = len(wl.plans) == 1
     ncls = wl.spec.op_classes
-    worst, n_or, n_band_tot, t_or = 0.0, 0, 0, 0.0
+    stats = {"worst": 0.0, "n_or": 0, "n_band": 0, "t_or": 0.0}
+    _free()
     for b in range(n_batches):
-        t0 = b * n
-        d = device_workload(wl, t0=t0, n=n, placement=wl.placement)
-        kv, ops = d["kv"], d["ops"]
-        sub = np.arange(0, n, k, dtype=np.int64)
-        if sub[-1] != n - 1:
-            sub = np.append(sub, n - 1)                   # and the batch's last tuple
-        tic = time.perf_counter()
-        m_or, c_or = fullsize.oracle_scores(wl, d, t0, sub)
-        t_or += time.perf_counter() - tic
-        n_or += len(sub)
-        gold_sub = parity.gold_from_oracle(m_or, c_or, wl.gold_variant, ncls)
-        gold = d["gold"].clone()                          # latent labels off the oracle subset
-        gold[:, torch.from_numpy(sub).cuda()] = torch.from_numpy(gold_sub).cuda()
-        # (1) the bench launch: every tuple of the resident batch
-        m_full, c_full, cnt_full = ko.score_batch(kv, ops, wl.variants, plans=wl.plans, gold=gold)
-        torch.cuda.synchronize()
-        mf = m_full.cpu().numpy()[:, :, sub]
-        if not routed:
-            assert np.isfinite(m_full.cpu().numpy()).all()
-        mask = np.isfinite(mf) if routed else None
-        worst = max(worst, parity.assert_margins(mf, m_or, mask=mask))
-        parity.assert_classes(np.where(np.isfinite(mf), c_full.cpu().numpy()[:, :, sub], c_or),
-                              c_or, m_or, ncls)
-        if k == 1:
-            n_band_tot += parity.assert_counts(cnt_full.cpu().numpy(), m_or, c_or, mf,
-                                               c_full.cpu().numpy(), wl.plans, ncls, gold_sub)
-            mg_t, cg_t = m_full, c_full
-        else:
-            # (2) the subset as its own pass (tuple_idx): exact counts on exactly those tuples
-            idx = torch.from_numpy(sub.astype(np.int32)).cuda()
-            m_s, c_s, cnt_s = ko.score_batch(kv, ops, wl.variants, tuple_idx=idx, plans=wl.plans,
-                                             gold=gold)
-            torch.cuda.synchronize()
-            ms = m_s.cpu().numpy()[:, :, sub]
-            cs = c_s.cpu().numpy()[:, :, sub]
-            fin = np.isfinite(ms)
-            assert np.array_equal(np.isfinite(mf), fin)
-            assert np.array_equal(ms[fin], mf[fin]), "full-pass and subset-pass margins differ"
-            n_band_tot += parity.assert_counts(cnt_s.cpu().numpy(), m_or, c_or, ms, cs, wl.plans,
-                                               ncls, gold_sub)
-            mg_t = torch.from_numpy(ms).cuda()
-            cg_t = torch.from_numpy(cs).cuda()
-            del m_s, c_s
-        n_clear = _check_plans(ko, wl.plans, ncls, m_or, c_or, mg_t, cg_t, gold_sub, routed)
-        del d, kv, ops, m_full, c_full, mg_t, cg_t, gold
-        _free()
+        try:
+            n_clear = _one_batch(ko, wl, b, n, k, routed, ncls, stats)
+        except BaseException as e:      # drop the failed batch's 100+ GB of locals for the next case
+            traceback.clear_frames(e.__traceback__)
+            raise
+        finally:
+            _free()
+    worst, n_or, n_band_tot, t_or = stats["worst"], stats["n_or"], stats["n_band"], stats["t_or"]
     print(f"{name}: {n_or} tuples vs oracle ({t_or:.0f} s), max|dm| = {worst:.2e}, "
           f"band entries = {n_band_tot}, min clear tuples per plan = {n_clear}")
+
+
+def _one_batch(ko, wl, b, n, k, routed, ncls, stats):
+    t0 = b * n
+    d = device_workload(wl, t0=t0, n=n, placement=wl.placement)
+    kv, ops = d["kv"], d["ops"]
+    sub = np.arange(0, n, k, dtype=np.int64)
+    if sub[-1] != n - 1:
+        sub = np.append(sub, n - 1)                   # and the batch's last tuple
+    tic = time.perf_counter()
+    m_or, c_or = fullsize.oracle_scores(wl, d, t0, sub)
+    stats["t_or"] += time.perf_counter() - tic
+    stats["n_or"] += len(sub)
+    gold_sub = parity.gold_from_oracle(m_or, c_or, wl.gold_variant, ncls)
+    gold = d["gold"].clone()                          # latent labels off the oracle subset
+    gold[:, torch.from_numpy(sub).cuda()] = torch.from_numpy(gold_sub).cuda()
+    # (1) the bench launch: every tuple of the resident batch
+    m_full, c_full, cnt_full = ko.score_batch(kv, ops, wl.variants, plans=wl.plans, gold=gold)
+    torch.cuda.synchronize()
+    mf = m_full.cpu().numpy()[:, :, sub]
+    if not routed:
+        assert np.isfinite(m_full.cpu().numpy()).all()
+    mask = np.isfinite(mf) if routed else None
+    stats["worst"] = max(stats["worst"], parity.assert_margins(mf, m_or, mask=mask))
+    parity.assert_classes(np.where(np.isfinite(mf), c_full.cpu().numpy()[:, :, sub], c_or),
+                          c_or, m_or, ncls)
+    if k == 1:
+        stats["n_band"] += parity.assert_counts(cnt_full.cpu().numpy(), m_or, c_or, mf,
+                                           c_full.cpu().numpy(), wl.plans, ncls, gold_sub)
+        mg_t, cg_t = m_full, c_full
+    else:
+        # (2) the subset as its own pass (tuple_idx): exact counts on exactly those tuples
+        idx = torch.from_numpy(sub.astype(np.int32)).cuda()
+        m_s, c_s, cnt_s = ko.score_batch(kv, ops, wl.variants, tuple_idx=idx, plans=wl.plans,
+                                         gold=gold)
+        torch.cuda.synchronize()
+        ms = np.ascontiguousarray(m_s.cpu().numpy()[:, :, sub])
+        cs = np.ascontiguousarray(c_s.cpu().numpy()[:, :, sub])
+        fin = np.isfinite(ms)
+        assert np.array_equal(np.isfinite(mf), fin)
+        assert np.array_equal(ms[fin], mf[fin]), "full-pass and subset-pass margins differ"
+        stats["n_band"] += parity.assert_counts(cnt_s.cpu().numpy(), m_or, c_or, ms, cs, wl.plans,
+                                           ncls, gold_sub)
+        mg_t = torch.from_numpy(ms).cuda()
+        cg_t = torch.from_numpy(cs).cuda()
+        del m_s, c_s
+    n_clear = _check_plans(ko, wl.plans, ncls, m_or, c_or, mg_t, cg_t, gold_sub, routed)
+    del d, kv, ops, m_full, c_full, mg_t, cg_t, gold
+    return n_clear
