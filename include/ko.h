@@ -224,16 +224,24 @@ ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, con
  * recurrences of Eqs. accept-i / reject-i / unsure-i, plan accept mass = product over the plan's
  * operators, soft TP / FP / FN (Eqs. 5–7) and cost Σ σ_i c_i · (mass reaching stage i) — and the
  * exact derivatives of these four sums w.r.t. every stage's (s_i, θ⁻_i, θ⁺_i) at the plan's
- * thresholds.  Filter operators only (maps: KO_EUNSUPPORTED).
+ * thresholds.  Map-classify operators (output-tuple selection): a non-final map stage
+ * resolves the mass u·σ_i·sigmoid((m − θ⁺)/τ) (finals: all of it) with the stage's argmax class;
+ * maps never reject (Q13); TP counts a tuple's plan-output mass times, per map, the mass resolved
+ * to its gold class, FP = output mass − TP, FN = gold mass − TP (a wrong value is one FP and one FN).
  * pick_scores, stage_cost: HOST double [plan->n_stages]; tau > 0; n_classes: host [n_ops].
+ * classes: device int32 [n_ops][n_variants][n_tuples] argmax classes (required iff the plan has a
+ *      map stage, else may be NULL); gold: device uint8 [n_ops][n_tuples] (filters 0/1, maps the
+ *      class) or NULL.
  * out: DEVICE double [4 + 12·n_stages] = {TP, FP, FN, cost} then, for q in (TP, FP, FN, cost),
  *      d q / d(s_i, θ⁻_i, θ⁺_i) at index 4 + q·3·n_stages + 3i + {0,1,2} (finals: d/ds = d/dθ⁻ = 0,
- *      the threshold derivative is reported on θ⁺).  Sums are fp64 in a fixed order
- *      (bitwise reproducible).  workspace: >= ko_soft_workspace_size(n_stages, n_tuples) bytes. */
+ *      the threshold derivative is reported on θ⁺; map stages: d/dθ⁻ = 0; a final map stage has
+ *      no parameters).  Sums are fp64 in a fixed order (bitwise reproducible).
+ *      workspace: >= ko_soft_workspace_size(n_stages, n_tuples) bytes.                        */
 ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const double* stage_cost,
-                        double tau, const float* margins, const int32_t* n_classes, int32_t n_ops,
-                        int32_t n_variants, int64_t n_tuples, const uint8_t* gold, double* out,
-                        void* workspace, size_t workspace_bytes, void* stream);
+                        double tau, const float* margins, const int32_t* classes,
+                        const int32_t* n_classes, int32_t n_ops, int32_t n_variants,
+                        int64_t n_tuples, const uint8_t* gold, double* out, void* workspace,
+                        size_t workspace_bytes, void* stream);
 size_t ko_soft_workspace_size(int32_t n_stages, int64_t n_tuples);
 
 /* Bytes of device workspace ko_score_batch needs for this shape (n_work = number of tuples it

@@ -84,7 +84,7 @@ def _load():
     L.ko_build_importance_order.restype = ctypes.c_int
     L.ko_embed_scores.argtypes = [P, I32, I64, P, I32, P, I32, I32, I32, P, I64, P, P]
     L.ko_embed_scores.restype = ctypes.c_int
-    L.ko_soft_stats.argtypes = [P, P, P, ctypes.c_double, P, P, I32, I32, I64, P, P, P,
+    L.ko_soft_stats.argtypes = [P, P, P, ctypes.c_double, P, P, P, I32, I32, I64, P, P, P,
                                 ctypes.c_size_t, P]
     L.ko_soft_stats.restype = ctypes.c_int
     L.ko_soft_workspace_size.argtypes = [I32, I64]
@@ -328,7 +328,7 @@ def embed_scores(item_emb, op_emb, op_ids: Sequence[int], margins, variant: int,
 
 def soft_stats(plan: Sequence[Stage], pick_scores: Sequence[float], stage_cost: Sequence[float],
                tau: float, margins, n_classes: Sequence[int], gold=None, out=None,
-               workspace=None, stream=None):
+               workspace=None, stream=None, classes=None):
     """ko_soft_stats: relaxed TP/FP/FN/cost and their Jacobian w.r.t. (s_i, θ⁻_i, θ⁺_i).
     Returns a device fp64 tensor [4 + 12·S] (see include/ko.h for the layout)."""
     import torch
@@ -342,7 +342,7 @@ def soft_stats(plan: Sequence[Stage], pick_scores: Sequence[float], stage_cost: 
     pk = (ctypes.c_double * S)(*[float(x) for x in pick_scores])
     cs = (ctypes.c_double * S)(*[float(x) for x in stage_cost])
     nc = (ctypes.c_int32 * n_ops)(*[int(c) for c in n_classes])
-    rc = _lib.ko_soft_stats(make_plans([plan]), pk, cs, float(tau), _dp(margins), nc, n_ops,
+    rc = _lib.ko_soft_stats(make_plans([plan]), pk, cs, float(tau), _dp(margins), _ptr(classes), nc, n_ops,
                             n_var, n, _ptr(gold), _dp(out), _dp(workspace),
                             workspace.numel(), _stream(stream))
     _check(rc)

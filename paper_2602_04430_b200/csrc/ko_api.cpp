@@ -886,9 +886,10 @@ size_t ko_soft_workspace_size(int32_t n_stages, int64_t n_tuples) {
 }
 
 ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const double* stage_cost,
-                        double tau, const float* margins, const int32_t* n_classes, int32_t n_ops,
-                        int32_t n_variants, int64_t n_tuples, const uint8_t* gold, double* out,
-                        void* workspace, size_t workspace_bytes, void* stream) {
+                        double tau, const float* margins, const int32_t* classes,
+                        const int32_t* n_classes, int32_t n_ops, int32_t n_variants,
+                        int64_t n_tuples, const uint8_t* gold, double* out, void* workspace,
+                        size_t workspace_bytes, void* stream) {
   g_launches = 0;
   if (!plan || !pick_scores || !stage_cost || !margins || !n_classes || !out || !workspace)
     return fail(KO_EINVAL, "ko_soft_stats: NULL argument");
@@ -901,8 +902,10 @@ ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const do
   ko::SoftParams sp;
   std::memset(&sp, 0, sizeof(sp));
   for (int i = 0; i < plan->n_stages; ++i) {
-    if (n_classes[plan->stage[i].op] > 1)
-      return fail(KO_EUNSUPPORTED, "ko_soft_stats: stage %d is a map operator (filters only)", i);
+    if (n_classes[plan->stage[i].op] > 1) {
+      if (!classes) return fail(KO_EINVAL, "ko_soft_stats: stage %d is a map stage: classes required", i);
+      sp.is_map[plan->stage[i].op] = 1;
+    }
     if (!std::isfinite(pick_scores[i]) || !std::isfinite(stage_cost[i]))
       return fail(KO_EINVAL, "stage %d: non-finite pick score or cost", i);
     sp.pick[i] = pick_scores[i];
@@ -915,6 +918,7 @@ ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const do
   sp.plan = *plan;
   sp.tau = tau;
   sp.margins = margins;
+  sp.classes = classes;
   sp.n_ops = n_ops;
   sp.n_variants = n_variants;
   sp.n_tuples = n_tuples;

@@ -213,8 +213,10 @@ struct SoftParams {
   const float* margins;  // [n_ops][n_variants][n_tuples]
   int32_t n_ops, n_variants;
   int64_t n_tuples;
-  const uint8_t* gold;   // [n_ops][n_tuples] or NULL
+  const uint8_t* gold;   // [n_ops][n_tuples] or NULL (filters 0/1, maps the class)
+  const int32_t* classes;  // [n_ops][n_variants][n_tuples] argmax classes (maps) or NULL
   int32_t referenced[kMaxOps];
+  int32_t is_map[kMaxOps];  // referenced op with n_classes > 1
   double* items;         // workspace [3·S + 1][4][n_tuples]
   double* partials;      // workspace [4·(3·S + 1)][16]: per-chunk sums of the items
 };

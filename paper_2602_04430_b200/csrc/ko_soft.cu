@@ -9,8 +9,12 @@
 // summed per output in a fixed order (fp64), so results are bitwise reproducible.  Equations (same order as oracle/soft.py):
 //   σ_i = sigmoid(s_i/τ) (finals: 1);  π_i = softmax([m − θ⁺, θ⁻ − m, 0]/τ) (finals: 2-way
 //   sigmoid((m − θ⁺)/τ));  a_i = a + u σ π_acc, r_i = r + u σ π_rej, u = 1 − a − r per op;
-//   cost += σ_i c_i u_{op_i} Π_{o'≠op_i}(1 − r_{o'});  A = Π_o a_o;  TP = Σ A g, FP = Σ A(1−g),
-//   FN = Σ (1−A) g with g = Π_o gold_o.
+//   cost += σ_i c_i u_{op_i} Π_{o'≠op_i}(1 − r_{o'});  A = Π_o a_o;  TP = Σ T g, FP = Σ (A − T g),
+//   FN = Σ (g − T g) with g = Π_filters gold_o and T = Π_filters a_o · Π_maps κ_o.
+// Map-classify stages (output-tuple selection; maps never reject, Q13): a non-final
+// stage resolves u σ_i ρ_i, ρ_i = sigmoid((m − θ⁺)/τ) (finals: σ = ρ = 1), and the op's correct
+// mass κ_o gains that amount when the stage's class equals the gold class (a wrong value is one
+// FP and one FN).  For filter-only plans T = A and the sums reduce to A g, A(1−g), (1−A) g.
 #include <algorithm>
 
 #include "ko_internal.h"
@@ -63,14 +67,27 @@ __global__ void soft_tuple_kernel(const __grid_constant__ SoftParams p) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     double vs[SM], va[SM], vr[SM], ds[SM], dalo[SM], dahi[SM], drlo[SM], drhi[SM];
+    bool ok[SM];  // map stages: the stage's class equals the gold class
 #pragma unroll
     for (int i = 0; i < SM; ++i) {
       vs[i] = 1.0; va[i] = vr[i] = ds[i] = dalo[i] = dahi[i] = drlo[i] = drhi[i] = 0.0;
+      ok[i] = false;
       if (i >= S) continue;
       const ko_stage& st = p.plan.stage[i];
-      const double m = (double)p.margins[((size_t)st.op * p.n_variants + st.variant) * n + t];
+      const size_t mi = ((size_t)st.op * p.n_variants + st.variant) * n + t;
+      const double m = (double)p.margins[mi];
       const double hi = (double)st.theta_hi, lo = (double)st.theta_lo;
-      if (st.is_final) {
+      if (p.is_map[st.op]) {
+        ok[i] = p.gold && p.classes[mi] == (int32_t)p.gold[(size_t)st.op * n + t];
+        if (st.is_final) {
+          va[i] = 1.0;                                         // resolves all that reaches it
+        } else {
+          const Dual sg = dsigmoid(itau * mk(p.pick[i], 1.0));  // seeded in s
+          vs[i] = sg.v; ds[i] = sg.d;
+          const Dual pa = dsigmoid(itau * (mk(m) - mk(hi, 1.0)));  // ρ, seeded in θ⁺
+          va[i] = pa.v; dahi[i] = pa.d;
+        }
+      } else if (st.is_final) {
         const Dual pa = dsigmoid(itau * (mk(m) - mk(hi, 1.0)));  // seeded in θ⁺
         va[i] = pa.v; vr[i] = 1.0 - pa.v; dahi[i] = pa.d; drhi[i] = -pa.d;
       } else {
@@ -86,13 +103,13 @@ __global__ void soft_tuple_kernel(const __grid_constant__ SoftParams p) {
     double g = 1.0;
 #pragma unroll
     for (int o = 0; o < kMaxOps; ++o)
-      if (o < p.n_ops && p.referenced[o])
+      if (o < p.n_ops && p.referenced[o] && !p.is_map[o])
         g *= p.gold ? (double)(p.gold[(size_t)o * n + t] == 1) : 0.0;
     for (int k = 0; k < P; ++k) {
       const int seed_stage = k == 0 ? -1 : (k - 1) / 3, seed_field = k == 0 ? -1 : (k - 1) % 3;
-      Dual a[kMaxOps], r[kMaxOps];
+      Dual a[kMaxOps], r[kMaxOps], kap[kMaxOps];
 #pragma unroll
-      for (int o = 0; o < kMaxOps; ++o) { a[o] = mk(0.0); r[o] = mk(0.0); }
+      for (int o = 0; o < kMaxOps; ++o) { a[o] = mk(0.0); r[o] = mk(0.0); kap[o] = mk(0.0); }
       Dual cost = mk(0.0);
 #pragma unroll
       for (int i = 0; i < SM; ++i) {
@@ -111,20 +128,29 @@ __global__ void soft_tuple_kernel(const __grid_constant__ SoftParams p) {
         }
         const Dual u = mk(1.0) - ao - ro;
         cost = cost + p.stage_cost[i] * (sig * u * alive);
-        const Dual na = ao + u * sig * pa, nr = ro + u * sig * pr;
+        const Dual res = u * sig * pa;
+        const Dual na = ao + res, nr = ro + u * sig * pr;
 #pragma unroll
         for (int o2 = 0; o2 < kMaxOps; ++o2)
-          if (o2 == o) { a[o2] = na; r[o2] = nr; }
+          if (o2 == o) {
+            a[o2] = na;
+            r[o2] = nr;
+            if (ok[i]) kap[o2] = kap[o2] + res;
+          }
       }
-      Dual A = mk(1.0);
+      Dual A = mk(1.0), T = mk(1.0);
 #pragma unroll
       for (int o = 0; o < kMaxOps; ++o)
-        if (o < p.n_ops && p.referenced[o]) A = A * a[o];
+        if (o < p.n_ops && p.referenced[o]) {
+          A = A * a[o];
+          T = T * (p.is_map[o] ? kap[o] : a[o]);
+        }
+      const Dual tg = g * T;
       double* dst = p.items + (size_t)k * 4 * n;
       const bool val = k == 0;
-      dst[0 * n + t] = val ? A.v * g : A.d * g;
-      dst[1 * n + t] = val ? A.v * (1.0 - g) : A.d * (1.0 - g);
-      dst[2 * n + t] = val ? (1.0 - A.v) * g : -A.d * g;
+      dst[0 * n + t] = val ? tg.v : tg.d;
+      dst[1 * n + t] = val ? A.v - tg.v : A.d - tg.d;
+      dst[2 * n + t] = val ? g - tg.v : -tg.d;
       dst[3 * n + t] = val ? cost.v : cost.d;
     }
   }

@@ -104,3 +104,72 @@ def test_gradients_match_finite_differences():
                 return soft.soft_stats([tuple(x) for x in pl], pk, tau, m, gold, cost)["values"]
             fd = (val(eps) - val(-eps)) / (2 * eps)
             assert np.allclose(jac[:, 3 * i + k], fd, rtol=1e-5, atol=1e-6), (i, field)
+
+
+# ---- map operators ---------------------------------------------
+def test_fever_coughing_soft_selection():
+    """candidates o₁ → "fever" (wrong), o₂ → "coughing" (gold); σ(o₁) = 0.3 leaves 0.7
+    of the mass for o₂ (the final stage) ⇒ tp 0.7, fp 0.3 (and fn 0.3: a wrong value is one FP
+    and one FN).  σ → 1 (choosing o₁) ⇒ tp 0, fp 1; σ → 0 (choosing o₂) ⇒ tp 1."""
+    tau = 1e-3
+    m = np.array([[[8.0], [8.0]]])                       # both confident (gap ≫ θ⁺ = 1)
+    cls = np.array([[[1], [2]]])                         # o₁: class 1 "fever", o₂: 2 "coughing"
+    gold = np.array([[2]])
+    plan = [(0, 0, 1.0, 1.0, 0), (0, 1, 0.0, 0.0, 1)]
+    for sig1, tp in ((0.3, 0.7), (1 - 1e-12, 0.0), (1e-12, 1.0)):
+        s1 = tau * np.log(sig1 / (1 - sig1))
+        v = soft.soft_stats(plan, [s1, 0.0], tau, m, gold, [1.0, 5.0], cls, [4])["values"]
+        assert np.allclose(v[:3], [tp, 1 - tp, 1 - tp], atol=1e-9)
+        assert abs(v[3] - (sig1 * 1.0 + (1 - sig1) * 5.0)) < 1e-9     # σ-scaled cost (Q10)
+
+
+def _map_problem(seed=0, n=400):
+    rng = np.random.default_rng(seed)
+    m = (np.round(rng.normal(0, 2, size=(3, 2, n)) * 8) + 0.5) / 8
+    m[1] = np.abs(m[1])                                  # map margins are top-1/top-2 gaps ≥ 0
+    cls = rng.integers(0, 4, size=(3, 2, n)).astype(np.int32)
+    cls[[0, 2]] = 0
+    gold = np.stack([rng.random(n) < 0.5, rng.integers(0, 4, n), rng.random(n) < 0.5]).astype(np.uint8)
+    plan = [(0, 0, -1.0, 0.7, 0), (0, 1, 0.0, 0.0, 1), (1, 0, 0.5, 0.5, 0), (1, 1, 0.0, 0.0, 1),
+            (2, 0, -0.4, 0.4, 0), (2, 1, 0.1, 0.1, 1)]
+    return m, cls, gold, plan
+
+
+@pytest.mark.parametrize("picks", [(10, 10, 10), (10, -10, 10), (-10, 10, -10)])
+def test_map_plan_tau_to_zero_equals_hard_counts(picks):
+    m, cls, gold, plan = _map_problem()
+    pick = [picks[0], 0, picks[1], 0, picks[2], 0]
+    cost = [1.0, 10.0, 2.0, 12.0, 1.5, 9.0]
+    v = soft.soft_stats(plan, pick, 1e-4, m, gold, cost, cls, [1, 4, 1])["values"]
+    keep = [i for i, st in enumerate(plan) if st[4] or pick[i] > 0]
+    cnt = oracle.run_plans([[plan[i] for i in keep]], m, cls, [1, 4, 1], gold)[0]
+    hard_cost = sum(cnt[5 + 4 * k] * cost[i] for k, i in enumerate(keep))
+    assert np.allclose(v, [cnt[0], cnt[1], cnt[2], hard_cost], atol=1e-6)
+    g = (gold[0] & gold[2]).sum()
+    assert abs(v[0] + v[2] - g) < 1e-6                   # tp + fn = gold mass (S:266)
+
+
+def test_map_plan_gradients_match_finite_differences():
+    m, cls, gold, plan = _map_problem(3, n=80)
+    pick = [0.3, 0.0, -0.2, 0.0, 0.1, 0.0]
+    tau, cost = 0.6, [1.0, 10.0, 2.0, 12.0, 1.5, 9.0]
+    jac = soft.soft_stats(plan, pick, tau, m, gold, cost, cls, [1, 4, 1])["jacobian"]
+    eps = 2.0 ** -20
+    assert np.all(jac[:, 3 * 2 + 1] == 0)                # maps ignore θ⁻
+    assert np.all(jac[:, 3 * 3: 3 * 4] == 0)             # a final map stage has no parameters
+    for i, field in [(2, "s"), (2, "hi"), (0, "hi"), (4, "lo")]:
+        def val(delta):
+            pk = list(pick); pl = [list(st) for st in plan]
+            if field == "s":
+                pk[i] += delta
+            elif field == "lo":
+                pl[i][2] += delta
+            else:
+                pl[i][3] += delta
+                if plan[i][0] == 1:
+                    pl[i][2] += delta                    # map stage: keep θ⁻ ≤ θ⁺
+            return soft.soft_stats([tuple(x) for x in pl], pk, tau, m, gold, cost, cls,
+                                   [1, 4, 1])["values"]
+        fd = (val(eps) - val(-eps)) / (2 * eps)
+        k = {"s": 0, "lo": 1, "hi": 2}[field]
+        assert np.allclose(jac[:, 3 * i + k], fd, rtol=1e-5, atol=1e-6), (i, field)

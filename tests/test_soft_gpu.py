@@ -42,10 +42,31 @@ def test_soft_stats_parity(ko, tau):
     assert torch.equal(out, out2)                      # fixed-order sums: bitwise reproducible
 
 
-def test_soft_stats_rejects_maps(ko):
-    m = torch.zeros((1, 1, 4), device="cuda")
-    with pytest.raises(ko.KoError, match="map"):
-        ko.soft_stats([(0, 0, 0.0, 0.0, 1)], [0.0], [1.0], 1.0, m, [3])
+@pytest.mark.parametrize("tau", [1.0, 0.05])
+def test_soft_stats_map_plan_parity(ko, tau):
+    """Filter → 4-class map → filter cascades (C4's shape) relaxed with the map's output-tuple
+    selection, against the oracle: values and the Jacobian."""
+    rng = np.random.default_rng(int(tau * 100) + 3)
+    n = 6000
+    m = rng.normal(0, 2, size=(3, 2, n)).astype(np.float32)
+    m[1] = np.abs(m[1])
+    cls = rng.integers(0, 4, size=(3, 2, n)).astype(np.int32)
+    cls[[0, 2]] = 0
+    gold = np.stack([rng.random(n) < 0.5, rng.integers(0, 4, n), rng.random(n) < 0.5]).astype(np.uint8)
+    plan = [(0, 0, -1.0, 0.7, 0), (0, 1, 0.0, 0.0, 1), (1, 0, 0.5, 0.5, 0), (1, 1, 0.0, 0.0, 1),
+            (2, 0, -0.4, 0.4, 0), (2, 1, 0.1, 0.1, 1)]
+    pick = [0.3, 0.0, -0.2, 0.0, 0.1, 0.0]
+    cost = [1.0, 10.0, 2.0, 12.0, 1.5, 9.0]
+    exp = soft.soft_stats(plan, pick, tau, m.astype(np.float64), gold, cost, cls, [1, 4, 1])
+    out = ko.soft_stats(plan, pick, cost, tau, torch.from_numpy(m).cuda(), [1, 4, 1],
+                        gold=torch.from_numpy(gold).cuda(), classes=torch.from_numpy(cls).cuda())
+    got = out.cpu().numpy()
+    assert np.allclose(got[:4], exp["values"], rtol=1e-10, atol=1e-9)
+    jac = got[4:].reshape(4, 3 * len(plan))
+    assert np.allclose(jac, exp["jacobian"], rtol=1e-8,
+                       atol=1e-10 * max(np.abs(exp["jacobian"]).max(), 1.0))
+    with pytest.raises(ko.KoError, match="classes"):
+        ko.soft_stats(plan, pick, cost, tau, torch.from_numpy(m).cuda(), [1, 4, 1])
 
 
 @pytest.mark.parametrize("tr,tpr", [(0.05, 0.05), (0.99, 0.99)])
