@@ -66,6 +66,8 @@ def lib():
         L.kg_fill_pool_device.restype = ctypes.c_int
         L.kg_read_stream.argtypes = [P, ctypes.c_int64, P, P]
         L.kg_read_stream.restype = ctypes.c_int
+        L.kg_gather_stream.argtypes = [P, ctypes.c_int32, P, ctypes.c_int64, P, P]
+        L.kg_gather_stream.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -232,3 +234,12 @@ def read_stream(d_buf: int, nbytes: int, d_sink: int, stream: int = 0) -> None:
     if lib().kg_read_stream(ctypes.c_void_p(d_buf), int(nbytes), ctypes.c_void_p(d_sink),
                             ctypes.c_void_p(stream)) != 0:
         raise RuntimeError("kg_read_stream failed")
+
+
+def gather_stream(d_base: int, row_bytes: int, d_idx: int, n: int, d_sink: int,
+                  stream: int = 0) -> None:
+    """Measurement helper (bench.py): one read of rows idx[0..n) of a device buffer (the
+    gathered-read ceiling of the embedding stage's tuple_idx path)."""
+    if lib().kg_gather_stream(ctypes.c_void_p(d_base), int(row_bytes), ctypes.c_void_p(d_idx),
+                              int(n), ctypes.c_void_p(d_sink), ctypes.c_void_p(stream)) != 0:
+        raise RuntimeError("kg_gather_stream failed")

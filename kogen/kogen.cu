@@ -303,6 +303,64 @@ __global__ void __launch_bounds__(128) read_stream_kernel(const uint8_t* __restr
   if (acc == 0x9e3779b9u) sink[blockIdx.x] = acc;  // practically never taken; keeps reads live
 }
 
+// Gathered-read stream: rows idx[0..n) of `row_bytes` each (16-byte multiple, ≤ 512) read
+// once through a per-warp ring of bulk copies, 32 rows per stage (one per lane) — the ceiling of
+// a kernel that reads a gathered row subset (ko_embed_scores with tuple_idx).
+__global__ void __launch_bounds__(128) gather_stream_kernel(const uint8_t* __restrict__ base,
+                                                            int row_bytes, const int32_t* __restrict__ idx,
+                                                            int64_t n, uint32_t* sink) {
+  extern __shared__ __align__(128) uint8_t gs_sm[];
+  __shared__ __align__(8) uint64_t bar[4][kRsStages];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int stage_bytes = 32 * row_bytes;
+  uint8_t* ring = gs_sm + warp * kRsStages * stage_bytes;
+  if (lane == 0)
+    for (int s = 0; s < kRsStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rs_su32(&bar[warp][s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t n_blk = (n + 31) / 32, nw = (int64_t)gridDim.x * 4;
+  int64_t next = (int64_t)blockIdx.x * 4 + warp, issued = 0, consumed = 0;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&]() {
+    const int s = (int)(issued % kRsStages);
+    const int64_t w = next * 32 + lane;
+    const int rows = (int)(n - next * 32 < 32 ? n - next * 32 : 32);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(rs_su32(&bar[warp][s])),
+                   "r"(rows * row_bytes) : "memory");
+    __syncwarp();
+    if (lane < rows)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+          "[%3], %4;" ::"r"(rs_su32(ring + s * stage_bytes + lane * row_bytes)),
+          "l"(base + (int64_t)idx[w] * row_bytes), "r"(row_bytes), "r"(rs_su32(&bar[warp][s])), "l"(pol)
+          : "memory");
+    ++issued;
+    next += nw;
+  };
+  for (int k = 0; k < kRsStages && next < n_blk; ++k) issue();
+  uint32_t acc = 0;
+  while (consumed < issued) {
+    const int s = (int)(consumed % kRsStages);
+    const uint32_t par = (uint32_t)((consumed / kRsStages) & 1);
+    uint32_t done = 0;
+    do {
+      asm volatile("{\n.reg .pred q;\nmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\nselp.u32 %0,1,0,q;\n}"
+                   : "=r"(done) : "r"(rs_su32(&bar[warp][s])), "r"(par) : "memory");
+    } while (!done);
+    acc ^= *(volatile uint32_t*)(ring + s * stage_bytes + lane * 4);
+    __syncwarp();
+    ++consumed;
+    if (next < n_blk) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue();
+    }
+  }
+  if (acc == 0x9e3779b9u) sink[blockIdx.x] = acc;  // practically never taken; keeps reads live
+}
+
 // Device fill: tuples t_begin .. t_begin+n_tuples-1 with device CSR (indptr has n_tuples+1
 // entries, may start at a non-zero offset), pages written into the device pool.
 int kg_fill_pool_device(const kg_cfg* c, int64_t t_begin, int64_t n_tuples, const int64_t* d_indptr,
@@ -341,6 +399,20 @@ int kg_read_stream(const void* d_buf, int64_t bytes, uint32_t* d_sink, void* str
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   read_stream_kernel<<<sms, 128, smem, (cudaStream_t)stream>>>((const uint8_t*)d_buf, bytes / kRsChunk,
                                                                d_sink);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+int kg_gather_stream(const void* d_base, int32_t row_bytes, const int32_t* d_idx, int64_t n,
+                     uint32_t* d_sink, void* stream) {
+  if (row_bytes % 16 != 0 || row_bytes < 16 || row_bytes > 512) return 1;
+  const int smem = 4 * kRsStages * 32 * row_bytes;
+  cudaFuncSetAttribute(gather_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_stream_kernel, 128, smem);
+  gather_stream_kernel<<<sms * (occ > 0 ? occ : 1), 128, smem, (cudaStream_t)stream>>>(
+      (const uint8_t*)d_base, row_bytes, d_idx, n, d_sink);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 

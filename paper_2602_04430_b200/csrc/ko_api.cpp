@@ -203,16 +203,10 @@ int max_entries(const ko_operator* ops, int n_ops) {
 // TMA descriptor of the pool: 5-D bf16 view, innermost first: (head_dim, 16 tokens, kv-head,
 // 2·layer + {K,V}, page); box (64, 16, 1, 2, 1) = the K and V rows of one kv-head of one layer of
 // one page for 64 head dims; SWIZZLE_128B (conflict-free fragment reads, see ko_kernels.cu).
-ko_status make_tmap(CUtensorMap* map, const ko_kv_cache* kv) {
-  const cuuint64_t D = (cuuint64_t)kv->head_dim;
-  cuuint64_t dims[5] = {D, 16, (cuuint64_t)kv->n_kv_heads, (cuuint64_t)(2 * kv->n_layers),
-                        (cuuint64_t)std::max<int64_t>(kv->n_pages, 1)};
-  cuuint64_t strides[4] = {D * 2, 16 * D * 2, (cuuint64_t)kv->n_kv_heads * 16 * D * 2,
-                           (cuuint64_t)(2 * kv->n_layers) * kv->n_kv_heads * 16 * D * 2};
-  cuuint32_t box[5] = {64, 16, 1, 2, 1};
-  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  // the driver entry point is resolved through the runtime, so libko.so does not link libcuda
-  // (the host-only parts of the ABI load on machines without a driver)
+// cuTensorMapEncodeTiled through the runtime's driver entry point (libko.so does not link libcuda,
+// so the host-only parts of the ABI load on machines without a driver); bf16, 128B swizzle
+ko_status encode_tmap(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims,
+                      const cuuint64_t* strides, const cuuint32_t* box, bool swizzle = true) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -222,13 +216,23 @@ ko_status make_tmap(CUtensorMap* map, const ko_kv_cache* kv) {
       return fail(KO_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
     encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
-                                      const_cast<void*>(kv->kv_pool), dims, strides, box, estr,
-                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims,
+                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(KO_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
   return KO_OK;
+}
+
+ko_status make_tmap(CUtensorMap* map, const ko_kv_cache* kv) {
+  const cuuint64_t D = (cuuint64_t)kv->head_dim;
+  cuuint64_t dims[5] = {D, 16, (cuuint64_t)kv->n_kv_heads, (cuuint64_t)(2 * kv->n_layers),
+                        (cuuint64_t)std::max<int64_t>(kv->n_pages, 1)};
+  cuuint64_t strides[4] = {D * 2, 16 * D * 2, (cuuint64_t)kv->n_kv_heads * 16 * D * 2,
+                           (cuuint64_t)(2 * kv->n_layers) * kv->n_kv_heads * 16 * D * 2};
+  cuuint32_t box[5] = {64, 16, 1, 2, 1};
+  return encode_tmap(map, kv->kv_pool, 5, dims, strides, box);
 }
 
 // Table packing (every scoring launch).  Lane group g owns S rows g (half 0) and g + 8 (half 1); W·V tile tt
@@ -820,26 +824,14 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
     const char* e = std::getenv("KO_EMB_TMAP");
     return e ? std::atoi(e) : 1;
   }();
-  if (emb_tmap && !tuple_idx && dim % 16 == 0 && dim <= 512 && n_tuples > 0 && n_tuples < (1ll << 31)) {
-    // contiguous rows: a 2-D tensor map (box 64 dims × 16 rows, 128B swizzle) over item_emb
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-      cudaDriverEntryPointQueryResult qr;
-      void* fn = nullptr;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
-          qr == cudaDriverEntryPointSuccess)
-        encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-    }
-    if (encode) {
-      cuuint64_t dims[2] = {(cuuint64_t)dim, (cuuint64_t)n_tuples};
-      cuuint64_t strides[1] = {(cuuint64_t)dim * 2};
-      cuuint32_t box[2] = {64, 16};
-      cuuint32_t estr[2] = {1, 1};
-      if (encode(&ep.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(item_emb), dims,
-                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-        ep.use_tmap = 1;
-    }
+  if (emb_tmap && dim % 16 == 0 && dim <= 512 && n_tuples > 0 && n_tuples < (1ll << 31)) {
+    // a 2-D tensor map over item_emb, 128B swizzle: contiguous rows in boxes of 64 dims × 16
+    // rows; gathered rows (tuple_idx) with tile::gather4, whose box is 64 dims × 1 row
+    cuuint64_t dims[2] = {(cuuint64_t)dim, (cuuint64_t)n_tuples};
+    cuuint64_t strides[1] = {(cuuint64_t)dim * 2};
+    cuuint32_t box[2] = {64, tuple_idx ? 1u : 16u};
+    // on failure the per-lane copy path runs (the message of the failed encode is dropped)
+    ep.use_tmap = encode_tmap(&ep.tmap, item_emb, 2, dims, strides, box) == KO_OK;
   }
   KO_LAUNCH(ko::launch_embed(ep, (cudaStream_t)stream));
   return KO_OK;
@@ -872,6 +864,25 @@ ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, con
   bp.inv_sqrt_d = 1.0 / std::sqrt((double)src->head_dim);
   bp.inv_2d = 1.0 / (2.0 * (double)src->head_dim);
   bp.n_pages = src->n_pages;
+  {
+    // 2-D views of both pools for the TMA loads, row gathers and stores (ko_build.cu)
+    const int64_t rows = src->n_pages * 2 * src->n_layers * src->n_kv_heads * KO_PAGE_TOKENS;
+    if (rows >= (1ll << 31))
+      return fail(KO_EUNSUPPORTED, "pool of %lld rows: the builder's TMA row coordinates are int32",
+                  (long long)rows);
+    const cuuint64_t D = (cuuint64_t)src->head_dim;
+    // score loads: 64-d × 16-row boxes, 128B swizzle (conflict-free per-token reads); row
+    // gathers and chunk stores: whole rows, unswizzled (the gathered rows are only copied)
+    struct { CUtensorMap* map; const void* base; cuuint32_t box_d, box_rows; bool swz; } views[3] = {
+        {&bp.tm_src, src->kv_pool, 64, 16, true}, {&bp.tm_row, src->kv_pool, (cuuint32_t)D, 1, false},
+        {&bp.tm_dst, dst_pool, (cuuint32_t)D, 16, false}};
+    for (auto& v : views) {
+      cuuint64_t dims[2] = {D, (cuuint64_t)std::max<int64_t>(rows, 1)};
+      cuuint64_t strides[1] = {D * 2};
+      cuuint32_t box[2] = {v.box_d, v.box_rows};
+      if ((st = encode_tmap(v.map, v.base, 2, dims, strides, box, v.swz)) != KO_OK) return st;
+    }
+  }
   KO_LAUNCH(ko::launch_build(bp, (cudaStream_t)stream));
   ++g_launches;  // launch_build: two kernels (short / long tuples)
   return KO_OK;

@@ -188,6 +188,10 @@ cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s);
 
 // importance-ordered cache builder (ko_build.cu)
 struct BuildParams {
+  // 2-D bf16 views [n_pages · 2·n_layers·n_kv_heads·16 rows][head_dim] of the pools:
+  alignas(64) CUtensorMap tm_src;  // source, box 64 d × 16 rows, 128B swizzle (score loads)
+  alignas(64) CUtensorMap tm_row;  // source, box D × 1 row, unswizzled (tile::gather4)
+  alignas(64) CUtensorMap tm_dst;  // destination, box D × 16 rows, unswizzled (chunk stores)
   const uint16_t* src_pool;
   const int64_t* indptr;
   const int32_t* src_ids;

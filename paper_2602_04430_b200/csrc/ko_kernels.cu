@@ -503,10 +503,16 @@ __device__ __forceinline__ void mma16816b(float (&d)[4], const uint32_t (&a)[4],
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int KSM, bool TM>  // k-steps of 16 dims (dim ≤ 16·KSM); TM: tensor-map loads
+// KSM: k-steps of 16 dims (dim ≤ 16·KSM).  TM: tensor-map loads into 128B-swizzled 16-row boxes —
+// contiguous rows as 64 × 16 boxes, or (G4) gathered rows (tuple_idx) with the sm_100 TMA row
+// gather `tile::gather4`: one op brings 4 arbitrary rows × 64 dims, so a 16-row block at dim 256
+// is 16 TMA ops instead of 512 per-lane cp.async copies, and the swizzled layout is the same as the
+// contiguous path's.  !TM: per-lane cp.async copies into padded rows (fallback).
+template <int KSM, bool TM, bool G4 = false>
 __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_constant__ EmbedParams p) {
   extern __shared__ __align__(128) uint8_t emb_sm[];
   __shared__ __align__(8) uint64_t bar[kEmbWarps][kEmbStages];
+  __shared__ int32_t s_tl[kEmbWarps][kEmbStages][kEmbRows];  // G4: the stage's tuple ids
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int dim = p.dim, KS = dim / 16;
@@ -578,14 +584,39 @@ __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_
   // (kept as the loaded int32: widening it at the load would wait for the load right there)
   auto load_tl = [&]() -> int32_t {
     const int64_t w = next * kEmbRows + lane;
-    return (!TM && next < n_blk && w < n) ? p.tuple_idx[w] : 0;
+    return ((!TM || G4) && next < n_blk && w < n) ? p.tuple_idx[w] : 0;
   };
   int32_t tl_next = load_tl();
   auto issue = [&]() {
     const int slot = issued % kEmbStages;
     const int64_t w0 = next * kEmbRows;
     const int rows = (int)(n - w0 < kEmbRows ? n - w0 : kEmbRows);
-    if constexpr (TM) {  // NB boxes (64 dims × 16 rows); out-of-range rows / dims are zero-filled
+    if constexpr (TM && G4) {
+      // 4 row groups × NB column boxes of gather4 (4 rows × 64 dims = 512 B each, at stage offset
+      // box·2048 + group·512, i.e. where a 16-row box puts those rows); lane j < 4 issues group j.
+      // Rows past the end of the list repeat the block's first tuple (loaded, never written out).
+      int32_t tl = tl_next;
+      const int32_t t0 = __shfl_sync(0xffffffffu, tl, 0);
+      if (lane >= rows) tl = t0;
+      if (lane < kEmbRows) s_tl[warp][slot][lane] = tl;
+      int32_t r4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) r4[i] = __shfl_sync(0xffffffffu, tl, (4 * lane + i) & 31);
+      if (lane == 0) mbar_expect_tx(&bar[warp][slot], (uint32_t)SB);
+      __syncwarp();
+      if (lane < 4)
+        for (int b = 0; b < NB; ++b)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(ring_s + slot * SB + b * kEmbRows * 128 + lane * 512),
+              "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(64 * b), "r"(r4[0]), "r"(r4[1]), "r"(r4[2]),
+              "r"(r4[3]), "r"(smem_u32(&bar[warp][slot])), "l"(policy)
+              : "memory");
+      ++issued;
+      next += nw;
+      tl_next = load_tl();
+      return;
+    } else if constexpr (TM) {  // NB boxes (64 dims × 16 rows); out-of-range rows / dims are zero-filled
       if (lane == 0) {
         mbar_expect_tx(&bar[warp][slot], (uint32_t)SB);
         for (int b = 0; b < NB; ++b)
@@ -632,28 +663,67 @@ __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_
     // output tuples of rows g, g + 8 (gathers: loaded before the wait, off the epilogue's path)
     const int64_t w0 = blk * kEmbRows;
     int32_t tout[2];  // int32 until used (see load_tl)
+    if constexpr (G4) {  // the ids the issue staged in shared memory (no global load here)
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr)
-      tout[hr] = w0 + g + 8 * hr < n ? (p.tuple_idx ? p.tuple_idx[w0 + g + 8 * hr] : (int32_t)0) : 0;
+      for (int hr = 0; hr < 2; ++hr) tout[hr] = s_tl[warp][slot][g + 8 * hr];
+    } else {
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr)
+        tout[hr] = w0 + g + 8 * hr < n ? (p.tuple_idx ? p.tuple_idx[w0 + g + 8 * hr] : (int32_t)0) : 0;
+    }
     mbar_wait(&bar[warp][slot], (consumed / kEmbStages) & 1u);
     const uint32_t st = ring_s + slot * SB + (TM ? 0u : lrow);
+    auto ldsm_ks = [&](uint32_t (&a)[4], int ks) {
+      if constexpr (TM) {
+        // box ks/4, 16-byte chunk 2·(ks%4) + (matrix ≥ 2), XORed with the row (128B swizzle)
+        const int r = (lane & 7) + 8 * ((lane >> 3) & 1);
+        const int c = 2 * (ks & 3) + (lane >> 4);
+        ldsm_x4(a, st + (ks >> 2) * (kEmbRows * 128) + r * 128 + ((c ^ (r & 7)) << 4));
+      } else {
+        ldsm_x4(a, st + 32 * ks);
+      }
+    };
     // two accumulator sets (even / odd k-steps) halve the MMA dependency chains
     float dd[2][4] = {}, g0[2][4] = {}, g1[2][4] = {};
+    if constexpr (KSM <= 16 && (G4 || !TM)) {
+      // gathered rows: the whole block's A fragments into registers first, so the stage goes
+      // back to the copy engine before the MMAs and the ring keeps more bytes in flight per SM
+      // (F = 0.5: 5.1 → 6.0 TB/s; the contiguous path ran 6.38 → 6.08 with it, so it keeps the
+      // interleaved order)
+      uint32_t af[KSM][4];
 #pragma unroll
-    for (int ks = 0; ks < KSM; ++ks) {
-      if (ks < KS) {
-        uint32_t a[4];
-        if constexpr (TM) {
-          // box ks/4, 16-byte chunk 2·(ks%4) + (matrix ≥ 2), XORed with the row (128B swizzle)
-          const int r = (lane & 7) + 8 * ((lane >> 3) & 1);
-          const int c = 2 * (ks & 3) + (lane >> 4);
-          ldsm_x4(a, st + (ks >> 2) * (kEmbRows * 128) + r * 128 + ((c ^ (r & 7)) << 4));
-        } else {
-          ldsm_x4(a, st + 32 * ks);
+      for (int ks = 0; ks < KSM; ++ks)
+        if (ks < KS) ldsm_ks(af[ks], ks);
+      __syncwarp();
+      ++consumed;
+      if (next < n_blk) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue();
+      }
+#pragma unroll
+      for (int ks = 0; ks < KSM; ++ks) {
+        if (ks < KS) {
+          mma16816b(dd[ks & 1], af[ks], bq[ks][0], bq[ks][1]);
+          mma16816b(g0[ks & 1], af[ks], af[ks][0], af[ks][2]);
+          mma16816b(g1[ks & 1], af[ks], af[ks][1], af[ks][3]);
         }
-        mma16816b(dd[ks & 1], a, bq[ks][0], bq[ks][1]);
-        mma16816b(g0[ks & 1], a, a[0], a[2]);
-        mma16816b(g1[ks & 1], a, a[1], a[3]);
+      }
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < KSM; ++ks) {
+        if (ks < KS) {
+          uint32_t a[4];
+          ldsm_ks(a, ks);
+          mma16816b(dd[ks & 1], a, bq[ks][0], bq[ks][1]);
+          mma16816b(g0[ks & 1], a, a[0], a[2]);
+          mma16816b(g1[ks & 1], a, a[1], a[3]);
+        }
+      }
+      __syncwarp();
+      ++consumed;
+      if (next < n_blk) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue();
       }
     }
 #pragma unroll
@@ -661,12 +731,6 @@ __global__ void __launch_bounds__(kEmbWarps * 32) embed_mma_kernel(const __grid_
       dd[0][i] += dd[1][i];
       g0[0][i] += g0[1][i];
       g1[0][i] += g1[1][i];
-    }
-    __syncwarp();
-    ++consumed;
-    if (next < n_blk) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue();
     }
     // squared norms of tuples g and g + 8 sit in lane (g, g/2): G0[g][g], G1[g + 8][g + 8]
     const float gsel0 = (g & 1) ? g0[0][1] : g0[0][0];
@@ -704,7 +768,11 @@ cudaError_t launch_embed(const EmbedParams& p, cudaStream_t s) {
       grid = std::min<int64_t>(grid, (n_blk + kEmbWarps - 1) / kEmbWarps);
       kern<<<(unsigned)std::max<int64_t>(grid, 1), kEmbWarps * 32, smem, s>>>(p);
     };
-    if (p.use_tmap) {
+    if (p.use_tmap && p.tuple_idx) {
+      if (p.dim <= 128) run(embed_mma_kernel<8, true, true>);
+      else if (p.dim <= 256) run(embed_mma_kernel<16, true, true>);
+      else run(embed_mma_kernel<32, true, true>);
+    } else if (p.use_tmap) {
       if (p.dim <= 128) run(embed_mma_kernel<8, true>);
       else if (p.dim <= 256) run(embed_mma_kernel<16, true>);
       else run(embed_mma_kernel<32, true>);
