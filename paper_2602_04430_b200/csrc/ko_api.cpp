@@ -10,12 +10,24 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
-#include <cstdlib>
 #include <cstring>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ko.h"
 #include "ko_internal.h"
+
+namespace {
+// NVTX range around every compute entry point (and each routed plan position), so an nsys /
+// ncu --nvtx timeline shows the library's calls; header-only NVTX3: a no-op without a tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 namespace {
 
@@ -430,6 +442,7 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
                          int64_t n_idx, float* margins, int32_t* classes, const ko_plan* plans,
                          int32_t n_plans, const uint8_t* gold, int64_t* counts, void* workspace,
                          size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("ko_score_batch");
   g_launches = 0;
   ko_status st;
   if ((st = validate_kv(kv)) != KO_OK) return st;
@@ -634,6 +647,9 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     if (launched(pos)) last_launch = pos;
   for (int pos = 0; pos < P.n_stages; ++pos) {
     if (!launched(pos)) continue;
+    char nv_name[48];
+    std::snprintf(nv_name, sizeof(nv_name), "ko_score_batch/routed position %d", pos);
+    NvtxRange nvtx_pos(nv_name);
     const int g = pos_group[pos];
     const bool walk_only = pos_round[pos] < 0;  // external stage at position 0
     const int r = std::max(pos_round[pos], 0);
@@ -703,6 +719,7 @@ ko_status ko_route(const ko_plan* plan, const float* margins, const int32_t* cla
                    const int32_t* n_classes, int32_t n_ops, int32_t n_variants, int64_t n_tuples,
                    int32_t stage, uint32_t* tuple_state, int32_t* worklist_out,
                    int64_t* worklist_len, const uint8_t* gold, int64_t* counts, void* stream) {
+  NvtxRange nvtx_("ko_route");
   g_launches = 0;
   if (!plan || !margins || !n_classes || !tuple_state || !counts)
     return fail(KO_EINVAL, "ko_route: NULL plan/margins/n_classes/tuple_state/counts");
@@ -756,6 +773,7 @@ ko_status ko_reduce_stats(const ko_plan* plans, int32_t n_plans, const float* ma
                           const int32_t* classes, const int32_t* n_classes, int32_t n_ops,
                           int32_t n_variants, int64_t n_tuples, const uint8_t* gold,
                           int64_t* counts, void* stream) {
+  NvtxRange nvtx_("ko_reduce_stats");
   g_launches = 0;
   if (!plans || !margins || !n_classes || !counts)
     return fail(KO_EINVAL, "ko_reduce_stats: NULL plans/margins/n_classes/counts");
@@ -793,6 +811,7 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
                           int32_t n_emb, const int32_t* op_ids, int32_t n_ops, int32_t variant,
                           int32_t n_variants, const int32_t* tuple_idx, int64_t n_idx,
                           float* margins, void* stream) {
+  NvtxRange nvtx_("ko_embed_scores");
   g_launches = 0;
   if (!item_emb || !op_emb || !op_ids || !margins) return fail(KO_EINVAL, "ko_embed_scores: NULL argument");
   if (dim < 8 || dim % 8 != 0 || dim > 1024) return fail(KO_EINVAL, "dim %d: multiple of 8 in [8,1024]", dim);
@@ -839,6 +858,7 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
 
 ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, const float* sigma2,
                                     void* dst_pool, const int32_t* dst_page_ids, void* stream) {
+  NvtxRange nvtx_("ko_build_importance_order");
   g_launches = 0;
   ko_status st;
   if ((st = validate_kv(src)) != KO_OK) return st;
@@ -901,6 +921,7 @@ ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const do
                         const int32_t* n_classes, int32_t n_ops, int32_t n_variants,
                         int64_t n_tuples, const uint8_t* gold, double* out, void* workspace,
                         size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("ko_soft_stats");
   g_launches = 0;
   if (!plan || !pick_scores || !stage_cost || !margins || !n_classes || !out || !workspace)
     return fail(KO_EINVAL, "ko_soft_stats: NULL argument");
