@@ -910,10 +910,8 @@ ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, con
 
 size_t ko_soft_workspace_size(int32_t n_stages, int64_t n_tuples) {
   if (n_stages < 1 || n_stages > KO_MAX_STAGES || n_tuples < 0) return 0;
-  // per-(direction, output, tuple) items, then the per-chunk sums of each output row
-  const size_t n = (size_t)std::max<int64_t>(n_tuples, 1);
-  return align256(sizeof(double) * (size_t)(3 * n_stages + 1) * 4 * n) +
-         align256(sizeof(double) * (size_t)(3 * n_stages + 1) * 4 * 16);
+  // the soft kernel's per-CTA partial sums of every (direction, output) row
+  return align256(sizeof(double) * (size_t)(3 * n_stages + 1) * 4 * (size_t)ko::soft_blocks(n_tuples));
 }
 
 ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const double* stage_cost,
@@ -955,12 +953,9 @@ ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const do
   sp.n_variants = n_variants;
   sp.n_tuples = n_tuples;
   sp.gold = gold;
-  sp.items = (double*)workspace;
-  sp.partials = (double*)((uint8_t*)workspace +
-                            align256(sizeof(double) * (size_t)(3 * plan->n_stages + 1) * 4 *
-                                     (size_t)std::max<int64_t>(n_tuples, 1)));
+  sp.partials = (double*)workspace;
   KO_LAUNCH(ko::launch_soft(sp, out, (cudaStream_t)stream));
-  g_launches += 2;  // launch_soft: three kernels (per-tuple items, chunk sums, in-order final sum)
+  ++g_launches;  // launch_soft: two kernels (per-tuple values with CTA sums, in-order final sum)
   return KO_OK;
 }
 

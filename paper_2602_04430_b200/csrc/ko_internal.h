@@ -221,10 +221,10 @@ struct SoftParams {
   const int32_t* classes;  // [n_ops][n_variants][n_tuples] argmax classes (maps) or NULL
   int32_t referenced[kMaxOps];
   int32_t is_map[kMaxOps];  // referenced op with n_classes > 1
-  double* items;         // workspace [3·S + 1][4][n_tuples]
-  double* partials;      // workspace [4·(3·S + 1)][16]: per-chunk sums of the items
+  double* partials;      // workspace [soft_blocks(n_tuples)][4·(3·S + 1)]: per-CTA sums
 };
 cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s);
+int soft_blocks(int64_t n_tuples);  // CTAs of the soft tuple kernel (sizes the workspace)
 
 // launchers (ko_kernels.cu); return cudaSuccess or the launch error
 cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);

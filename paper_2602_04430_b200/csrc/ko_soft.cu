@@ -5,8 +5,11 @@
 //
 // Per tuple the relaxed cascade is a short chain of scalar operations; derivatives are taken in
 // forward mode with dual numbers, one pass per parameter (3·S ≤ 24) over stage values computed
-// once (soft_stage_kernel, then soft_items_kernel).  Per-(direction, output, tuple) results go to a workspace and are
-// summed per output in a fixed order (fp64), so results are bitwise reproducible.  Equations (same order as oracle/soft.py):
+// once per tuple.  Each (direction, output) value is summed over the CTA right away — a fixed
+// warp-shuffle tree, then the 4 warps in order into a per-CTA fp64 accumulator — and a second
+// kernel adds the CTAs' partial sums in a fixed order, so results are bitwise reproducible and
+// nothing per tuple goes to memory (r01 wrote every (direction, output, tuple) item to a
+// workspace and summed it in two more launches).  Equations (same order as oracle/soft.py):
 //   σ_i = sigmoid(s_i/τ) (finals: 1);  π_i = softmax([m − θ⁺, θ⁻ − m, 0]/τ) (finals: 2-way
 //   sigmoid((m − θ⁺)/τ));  a_i = a + u σ π_acc, r_i = r + u σ π_rej, u = 1 − a − r per op;
 //   cost += σ_i c_i u_{op_i} Π_{o'≠op_i}(1 − r_{o'});  A = Π_o a_o;  TP = Σ T g, FP = Σ (A − T g),
@@ -58,21 +61,30 @@ __device__ __forceinline__ void dsoftmax3(Dual z0, Dual z1, Dual* p0, Dual* p1) 
 //       ∂π_a/∂θ⁺ = −π_a(1 − π_a)/τ,  ∂π_r/∂θ⁺ = π_a π_r/τ,
 //       ∂π_a/∂θ⁻ = −π_a π_r/τ,       ∂π_r/∂θ⁻ = π_r(1 − π_r)/τ
 //   finals: π_a = sigmoid((m − θ⁺)/τ), π_r = 1 − π_a: ∂π_a/∂θ⁺ = −π_a(1 − π_a)/τ = −∂π_r/∂θ⁺.
+constexpr int kSoftThreads = 128;
 template <int SM>  // ≥ the plan's stages
-__global__ void soft_tuple_kernel(const __grid_constant__ SoftParams p) {
+__global__ void __launch_bounds__(kSoftThreads) soft_tuple_kernel(const __grid_constant__ SoftParams p) {
+  __shared__ double s_acc[4 * (3 * SM + 1)];         // this CTA's sums, row = direction·4 + output
+  __shared__ double s_w[kSoftThreads / 32][4];        // per-warp sums of one direction
   const int S = p.plan.n_stages;
   const int P = 3 * S + 1;
   const double itau = 1.0 / p.tau;
   const int64_t n = p.n_tuples;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 4 * P; i += blockDim.x) s_acc[i] = 0.0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t iters = (n + stride - 1) / stride;  // the same for every thread (block sums)
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t t = it * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = t < n;
     double vs[SM], va[SM], vr[SM], ds[SM], dalo[SM], dahi[SM], drlo[SM], drhi[SM];
     bool ok[SM];  // map stages: the stage's class equals the gold class
 #pragma unroll
     for (int i = 0; i < SM; ++i) {
       vs[i] = 1.0; va[i] = vr[i] = ds[i] = dalo[i] = dahi[i] = drlo[i] = drhi[i] = 0.0;
       ok[i] = false;
-      if (i >= S) continue;
+      if (i >= S || !valid) continue;
       const ko_stage& st = p.plan.stage[i];
       const size_t mi = ((size_t)st.op * p.n_variants + st.variant) * n + t;
       const double m = (double)p.margins[mi];
@@ -103,7 +115,7 @@ __global__ void soft_tuple_kernel(const __grid_constant__ SoftParams p) {
     double g = 1.0;
 #pragma unroll
     for (int o = 0; o < kMaxOps; ++o)
-      if (o < p.n_ops && p.referenced[o] && !p.is_map[o])
+      if (valid && o < p.n_ops && p.referenced[o] && !p.is_map[o])
         g *= p.gold ? (double)(p.gold[(size_t)o * n + t] == 1) : 0.0;
     for (int k = 0; k < P; ++k) {
       const int seed_stage = k == 0 ? -1 : (k - 1) / 3, seed_field = k == 0 ? -1 : (k - 1) % 3;
@@ -146,66 +158,64 @@ __global__ void soft_tuple_kernel(const __grid_constant__ SoftParams p) {
           T = T * (p.is_map[o] ? kap[o] : a[o]);
         }
       const Dual tg = g * T;
-      double* dst = p.items + (size_t)k * 4 * n;
       const bool val = k == 0;
-      dst[0 * n + t] = val ? tg.v : tg.d;
-      dst[1 * n + t] = val ? A.v - tg.v : A.d - tg.d;
-      dst[2 * n + t] = val ? g - tg.v : -tg.d;
-      dst[3 * n + t] = val ? cost.v : cost.d;
+      double v4[4] = {val ? tg.v : tg.d, val ? A.v - tg.v : A.d - tg.d, val ? g - tg.v : -tg.d,
+                      val ? cost.v : cost.d};
+      // CTA sum of this direction's 4 outputs in a fixed order: shuffle tree, then warps 0..3
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!valid) v4[q] = 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v4[q] += __shfl_down_sync(0xffffffffu, v4[q], off);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s_w[warp][q] = v4[q];
+      }
+      __syncthreads();
+      if (threadIdx.x < 4) {
+        double a = s_w[0][threadIdx.x];
+        for (int w = 1; w < kSoftThreads / 32; ++w) a += s_w[w][threadIdx.x];
+        s_acc[k * 4 + threadIdx.x] += a;
+      }
+      __syncthreads();
     }
   }
+  for (int i = threadIdx.x; i < 4 * P; i += blockDim.x)
+    p.partials[(size_t)blockIdx.x * 4 * P + i] = s_acc[i];
 }
 
-// Fixed-order sums of the items: pass 1, kSoftChunks CTAs per output row each sum one contiguous
-// chunk (8 independent accumulators per thread, then a fixed tree); pass 2 adds a row's chunk
-// sums in chunk order.  Bitwise reproducible.
-constexpr int kSoftChunks = 16;
-__global__ void soft_reduce_kernel(const double* items, int64_t n, double* part, int n_rows) {
-  __shared__ double sh[256];
-  const int row = blockIdx.x / kSoftChunks, chunk = blockIdx.x % kSoftChunks;
+// The CTAs' partial sums, one warp per output row: lane j adds CTAs j, j + 32, ... in order,
+// then a fixed shuffle tree.  Bitwise reproducible (the grid size depends only on n_tuples).
+__global__ void soft_final_kernel(const double* part, int n_blocks, double* out, int n_rows, int S) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= n_rows) return;
-  const int64_t per = (n + kSoftChunks - 1) / kSoftChunks;
-  const int64_t b0 = chunk * per, b1 = min(n, b0 + per);
-  const double* src = items + (size_t)row * n;
-  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  int64_t i = b0 + threadIdx.x;
-  for (; i + 7 * 256 < b1; i += 8 * 256) {
+  double a = 0.0;
+  for (int b = lane; b < n_blocks; b += 32) a += part[(size_t)b * n_rows + row];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] += src[i + u * 256];
-  }
-  for (int u = 0; i < b1; i += 256, ++u) acc[u & 7] += src[i];
-  double a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-  sh[threadIdx.x] = a;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
-}
-
-__global__ void soft_final_kernel(const double* part, double* out, int n_rows, int S) {
-  for (int row = threadIdx.x; row < n_rows; row += blockDim.x) {
-    double a = 0.0;
-    for (int c = 0; c < kSoftChunks; ++c) a += part[row * kSoftChunks + c];
+  for (int off = 16; off > 0; off >>= 1) a += __shfl_down_sync(0xffffffffu, a, off);
+  if (lane == 0) {
     const int k = row / 4, q = row % 4;
     out[k == 0 ? q : 4 + q * 3 * S + (k - 1)] = a;
   }
 }
 
-
 }  // namespace
 
-cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s) {
+int soft_blocks(int64_t n_tuples) {  // the tuple kernel's grid: a function of n_tuples only
+  const int64_t b = std::min<int64_t>((n_tuples + kSoftThreads - 1) / kSoftThreads, 148 * 8);
+  return (int)std::max<int64_t>(b, 1);
+}
+
+cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s) {  // 2 launches
   const int S = p.plan.n_stages;
   const int P = 3 * S + 1;
-  int blocks = (int)std::min<int64_t>((p.n_tuples + 127) / 128, 148 * 16);
-  if (blocks < 1) blocks = 1;
-  if (S <= 2) soft_tuple_kernel<2><<<blocks, 128, 0, s>>>(p);
-  else if (S <= 4) soft_tuple_kernel<4><<<blocks, 128, 0, s>>>(p);
-  else soft_tuple_kernel<8><<<blocks, 128, 0, s>>>(p);
-  soft_reduce_kernel<<<4 * P * kSoftChunks, 256, 0, s>>>(p.items, p.n_tuples, p.partials, 4 * P);
-  soft_final_kernel<<<1, 128, 0, s>>>(p.partials, out, 4 * P, S);
+  const int blocks = soft_blocks(p.n_tuples);
+  if (S <= 2) soft_tuple_kernel<2><<<blocks, kSoftThreads, 0, s>>>(p);
+  else if (S <= 4) soft_tuple_kernel<4><<<blocks, kSoftThreads, 0, s>>>(p);
+  else soft_tuple_kernel<8><<<blocks, kSoftThreads, 0, s>>>(p);
+  soft_final_kernel<<<(4 * P + 3) / 4, 128, 0, s>>>(p.partials, blocks, out, 4 * P, S);
   return cudaGetLastError();
 }
 
