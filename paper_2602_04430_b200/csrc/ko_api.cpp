@@ -954,6 +954,21 @@ ko_status ko_soft_stats(const ko_plan* plan, const double* pick_scores, const do
   sp.n_tuples = n_tuples;
   sp.gold = gold;
   sp.partials = (double*)workspace;
+  for (int o = 0; o < n_ops; ++o)  // compact slots in op-id order (same product order)
+    if (sp.referenced[o]) {
+      sp.slot_op[sp.n_slots] = o;
+      sp.slot_is_map[sp.n_slots] = sp.is_map[o];
+      ++sp.n_slots;
+    }
+  for (int i = 0; i < plan->n_stages; ++i) {
+    for (int k = 0; k < sp.n_slots; ++k)
+      if (sp.slot_op[k] == plan->stage[i].op) sp.stage_slot[i] = k;
+    // parameters with an effect (ko.h: finals have only θ⁺, maps no θ⁻, a final map none)
+    const bool fin = plan->stage[i].is_final != 0, map = sp.is_map[plan->stage[i].op] != 0;
+    sp.dir_live[3 * i + 0] = !fin;
+    sp.dir_live[3 * i + 1] = !fin && !map;
+    sp.dir_live[3 * i + 2] = !(fin && map);
+  }
   KO_LAUNCH(ko::launch_soft(sp, out, (cudaStream_t)stream));
   ++g_launches;  // launch_soft: two kernels (per-tuple values with CTA sums, in-order final sum)
   return KO_OK;

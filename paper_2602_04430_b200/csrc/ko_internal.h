@@ -221,6 +221,11 @@ struct SoftParams {
   const int32_t* classes;  // [n_ops][n_variants][n_tuples] argmax classes (maps) or NULL
   int32_t referenced[kMaxOps];
   int32_t is_map[kMaxOps];  // referenced op with n_classes > 1
+  // compact operator slots: the plan's distinct operators in op-id order
+  int32_t n_slots;
+  int32_t slot_op[kMaxOps], slot_is_map[kMaxOps];
+  int32_t stage_slot[KO_MAX_STAGES];
+  int32_t dir_live[3 * KO_MAX_STAGES];  // direction 1 + 3i + f moves the outputs (0: exact zeros)
   double* partials;      // workspace [soft_blocks(n_tuples)][4·(3·S + 1)]: per-CTA sums
 };
 cudaError_t launch_soft(const SoftParams& p, double* out, cudaStream_t s);
