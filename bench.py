@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU work budget of the oracle sample (cpu_baseline / reference arm)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-gb", type=float, default=24.0,
                     help="pinned host memory per rank for the e2e batch")
     ap.add_argument("--embed-subset", type=float, default=0.0,
