@@ -214,7 +214,9 @@ ko_status ko_embed_scores(const void* item_emb, int32_t dim, int64_t n_tuples, c
  * rows, rank r to slot r % 16 of logical page r / 16, into dst_pool at pages dst_page_ids (same
  * CSR offsets src->page_indptr; same page geometry).  Slots past L_t are not written.
  * mu, sigma2: device fp32 [n_layers][n_kv_heads][head_dim].  Tuples longer than 4096 tokens are
- * skipped (not supported).  Asynchronous on `stream`.                                         */
+ * skipped (not supported).  Every byte moves by TMA over 2-D views of both pools
+ * ([n_pages · 2·n_layers·n_kv_heads·16 rows][head_dim]); a pool whose view has ≥ 2^31 rows
+ * returns KO_EUNSUPPORTED before any launch.  Asynchronous on `stream`.                       */
 ko_status ko_build_importance_order(const ko_kv_cache* src, const float* mu, const float* sigma2,
                                     void* dst_pool, const int32_t* dst_page_ids, void* stream);
 
