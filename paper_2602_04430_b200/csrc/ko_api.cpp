@@ -155,6 +155,8 @@ struct Workspace {
   int32_t* round_wl;              // [KO_MAX_STAGES][n_tuples] per-position worklists
   ko_plan* gplans;                // [KO_MAX_PLANS] device copy of the plans
   uint32_t* tuple_done;           // [n_tuples]
+  int* lpt_hist;                  // [4097] longest-first counting sort (grid mode)
+  int32_t* lpt_perm;              // [n_work] the work list in longest-first order
   float* rstate;                  // [n_ops groups][n_tuples][n_layers][Hkv][8][rstate_w]
   int rstate_w;
   size_t rstate_group;            // floats per group slice
@@ -191,6 +193,8 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int max_ent, int32_t n_ops,
   w.round_wl = (int32_t*)take(sizeof(int32_t) * nt * KO_MAX_STAGES);
   w.gplans = (ko_plan*)take(sizeof(ko_plan) * KO_MAX_PLANS);
   w.tuple_done = (uint32_t*)take(sizeof(uint32_t) * nt);
+  w.lpt_hist = (int*)take(sizeof(int) * 4097);
+  w.lpt_perm = (int32_t*)take(sizeof(int32_t) * (size_t)std::max<int64_t>(n_work, 1));
   // saved softmax states of the routed rounds: a group's table needs ≤ pow2(max entries per row)
   // tiles, so 4 + 2·that floats per lane group bound every group's state
   w.rstate_w = 4 + 2 * std::min(ko::kMaxTNT, pow2_at_least(std::max(max_ent, 1)));
@@ -496,7 +500,10 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     sp.n_ext = n_ext;
     for (int i = 0; i < n_ext; ++i) sp.ext_ids[i] = ext[i];
     if ((st = make_tmap(&sp.tmap, kv)) != KO_OK) return st;
-    sp.work = tuple_idx;
+    // longest-first work order (varlen tail balance; identity for a fixed-length batch)
+    KO_LAUNCH(ko::launch_lpt_order(tuple_idx, n_work, kv->seq_len, ws.lpt_hist, ws.lpt_perm, s));
+    g_launches += 2;  // launch_lpt_order: 3 kernels
+    sp.work = ws.lpt_perm;
     sp.work_len_host = n_work;
     sp.work_len_dev = nullptr;
     sp.margins = margins;

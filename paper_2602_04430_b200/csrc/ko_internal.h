@@ -246,6 +246,10 @@ cudaError_t launch_route_apply(const RouteParams& p, cudaStream_t s);  // apply 
 cudaError_t launch_route_plan(const RouteParams& p, cudaStream_t s);   // whole plan on margins
 cudaError_t launch_route_init(uint32_t* state, int64_t n, cudaStream_t s);
 cudaError_t launch_final_counts(const RouteParams& p, cudaStream_t s);  // TP/FP/FN from state
+// longest-first order of a work list (tuple ids, or 0..n−1 when work is NULL) into perm:
+// hist = workspace [4097] ints; 3 kernels (+ a memset)
+cudaError_t launch_lpt_order(const int32_t* work, int64_t n_work, const int32_t* seq_len,
+                             int* hist, int32_t* perm, cudaStream_t s);
 cudaError_t launch_reduce(const ReduceParams& p, cudaStream_t s);
 cudaError_t launch_fill_f32(float* p, float v, int64_t n, cudaStream_t s);
 

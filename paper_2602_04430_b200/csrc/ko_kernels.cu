@@ -828,6 +828,93 @@ cudaError_t launch_route_plan(const RouteParams& p, cudaStream_t s) {
   route_plan_kernel<<<num_sms() * 4, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
+// ---- Longest-first work order (grid mode): a counting sort of the work list by streamed pages,
+// descending, so the last work units a persistent kernel claims are short ones (the tail of a
+// varlen batch is one short unit instead of up to a 4096-token one).  Bucket = min(pages, 4095),
+// reversed; warp-aggregated atomics (a fixed-length batch has one bucket).  A batch with a single
+// bucket keeps the caller's order (identity), so fixed-length configs are unaffected.
+constexpr int kLptBuckets = 4096;
+__device__ __forceinline__ int lpt_bucket(const int32_t* seq_len, int64_t t) {
+  const int pages = (seq_len[t] + 15) >> 4;
+  return kLptBuckets - 1 - min(pages, kLptBuckets - 1);  // longest first
+}
+__global__ void lpt_hist_kernel(const int32_t* work, int64_t n_work, const int32_t* seq_len,
+                                int* hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - threadIdx.x < n_work;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool ok = i < n_work;
+    const int b = ok ? lpt_bucket(seq_len, work ? work[i] : i) : -1;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    if (!ok) continue;
+    const unsigned peers = __match_any_sync(act, b);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
+  }
+}
+// one CTA: exclusive scan of the buckets in place; hist[kLptBuckets] = number of non-empty buckets
+__global__ void __launch_bounds__(1024) lpt_scan_kernel(int* hist) {
+  __shared__ int s_part[1024];
+  __shared__ int s_ne[1024];
+  constexpr int per = kLptBuckets / 1024;
+  int v[per], sum = 0, ne = 0;
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    v[k] = hist[threadIdx.x * per + k];
+    sum += v[k];
+    ne += v[k] > 0;
+  }
+  s_part[threadIdx.x] = sum;
+  s_ne[threadIdx.x] = ne;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan of the thread sums
+    const int a = threadIdx.x >= off ? s_part[threadIdx.x - off] : 0;
+    const int c = threadIdx.x >= off ? s_ne[threadIdx.x - off] : 0;
+    __syncthreads();
+    s_part[threadIdx.x] += a;
+    s_ne[threadIdx.x] += c;
+    __syncthreads();
+  }
+  int run = s_part[threadIdx.x] - sum;
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    hist[threadIdx.x * per + k] = run;
+    run += v[k];
+  }
+  if (threadIdx.x == 1023) hist[kLptBuckets] = s_ne[1023];
+}
+__global__ void lpt_scatter_kernel(const int32_t* work, int64_t n_work, const int32_t* seq_len,
+                                   int* offs, int32_t* perm) {
+  const bool single = offs[kLptBuckets] <= 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - threadIdx.x < n_work;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool ok = i < n_work;
+    const int32_t t = ok ? (work ? work[i] : (int32_t)i) : 0;
+    if (single) {
+      if (ok) perm[i] = t;
+      continue;
+    }
+    const int b = ok ? lpt_bucket(seq_len, t) : -1;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    if (!ok) continue;
+    const unsigned peers = __match_any_sync(act, b);
+    const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&offs[b], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    perm[base + __popc(peers & ((1u << lane) - 1))] = t;
+  }
+}
+
+cudaError_t launch_lpt_order(const int32_t* work, int64_t n_work, const int32_t* seq_len,
+                             int* hist, int32_t* perm, cudaStream_t s) {  // 3 launches
+  cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int) * (kLptBuckets + 1), s);
+  if (e != cudaSuccess) return e;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n_work + 255) / 256, num_sms() * 4));
+  lpt_hist_kernel<<<blocks, 256, 0, s>>>(work, n_work, seq_len, hist);
+  lpt_scan_kernel<<<1, 1024, 0, s>>>(hist);
+  lpt_scatter_kernel<<<blocks, 256, 0, s>>>(work, n_work, seq_len, hist, perm);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_final_counts(const RouteParams& p, cudaStream_t s) {
   final_counts_kernel<<<num_sms() * 2, 256, 0, s>>>(p);
   return cudaGetLastError();
