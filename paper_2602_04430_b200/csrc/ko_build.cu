@@ -160,7 +160,10 @@ __global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_const
             tma_load_2d(ring_s + j * kBuildSlotBytes + b * 2048, &p.tm_src, 64 * b,
                         s_src[pg0 + j] * RP + row_k, &sbar, keep);
       }
-      mbar_wait(&sbar, sphase);
+      // one warp polls the round's barrier; the rest sleep in the CTA barrier instead of
+      // spinning on try_wait (the spin took 5 % of the issue slots the other CTAs need)
+      if (warp == 0) mbar_wait(&sbar, sphase);
+      __syncthreads();
       sphase ^= 1u;
       PROF_MARK(4);
       const int i = pg0 * 16 + threadIdx.x;
