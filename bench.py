@@ -316,6 +316,8 @@ def main():
             # NCCL logs each communicator's rank / nranks at init (visible in the run's stderr)
             os.environ["NCCL_DEBUG"] = os.environ.get("KO_NCCL_DEBUG", "INFO")
             os.environ["NCCL_DEBUG_SUBSYS"] = os.environ.get("KO_NCCL_DEBUG_SUBSYS", "INIT")
+            # NCCL logs to stdout by default: keep stdout for the one JSON line
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
