@@ -24,9 +24,11 @@ def test_bench_nccl_path_single_rank():
            "--no-cpu-baseline"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=280, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
-    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    out = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(out) == 1, out[:5]                        # stdout = exactly the one JSON line
+    line = json.loads(out[0])
     assert line["n_gpus"] == 1 and line["value"] > 0
-    assert "NCCL INFO" in r.stdout + r.stderr and "rank 0 of 1" in r.stderr
+    assert "NCCL INFO" in r.stderr and "nRanks 1" in r.stderr and "rank 0 of 1" in r.stderr
     assert line["counts_plan0"][3] > 0                   # counts survived the all-reduce
 
 
