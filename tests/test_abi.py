@@ -106,3 +106,19 @@ def test_binding_refuses_host_tensors():
     import paper_2602_04430_b200 as ko
     with pytest.raises(ValueError, match="CUDA"):
         ko._dp(torch.zeros(4))
+
+
+def test_builder_rejects_pools_beyond_its_tma_views():
+    """ko_build_importance_order moves every byte through 2-D TMA views of the pools whose row
+    coordinate is int32 (ko.h): a pool of >= 2^31 rows is refused with KO_EUNSUPPORTED before any
+    device work (checked here without a GPU: the pointers are never dereferenced)."""
+    import paper_2602_04430_b200 as ko
+    kv = _kv(head_dim=128, layers=2)
+    rows_per_page = 2 * 2 * 2 * 16                      # 2·layers·heads·16 rows of head_dim
+    kv.n_pages = (1 << 31) // rows_per_page + 1
+    fake = 1 << 20
+    rc = ko.lib().ko_build_importance_order(ctypes.byref(kv), ctypes.c_void_p(fake),
+                                            ctypes.c_void_p(fake), ctypes.c_void_p(fake),
+                                            ctypes.c_void_p(fake), None)
+    assert rc == 2, ko.last_error()                     # KO_EUNSUPPORTED
+    assert "int32" in ko.last_error()
