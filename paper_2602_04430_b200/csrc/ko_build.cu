@@ -82,8 +82,10 @@ constexpr size_t build_smem_bytes() {
 }
 
 // this kernel's units: MINT < L ≤ MAXT; SLOTS ring slots (one 16-token page of one head each)
+// (256, 4): the 64-register budget of 4 CTAs per SM; without the minimum ptxas kept 48 registers
+// and spilled two loop counters (same-box A/B: 6.59 → 6.43 ms)
 template <int MAXT, int MINT, int SLOTS, int kGatherWarps>
-__global__ void __launch_bounds__(kBuildThreads) build_kernel(const __grid_constant__ BuildParams p) {
+__global__ void __launch_bounds__(kBuildThreads, 4) build_kernel(const __grid_constant__ BuildParams p) {
   constexpr int kGatherSlots = SLOTS / kGatherWarps;  // per gather warp
   constexpr int kGatherAhead = kGatherSlots / 2;      // chunks a gather warp issues ahead
   extern __shared__ uint8_t bsm_raw[];
