@@ -684,6 +684,8 @@ def run_e2e(args, ko, torch, wl, d, ops, gold, plans, margins, classes, counts, 
         h_counts.copy_(counts, non_blocking=True)
         h_margins.copy_(margins, non_blocking=True)
 
+    # the resident pass's margins of the e2e batch, to check the streamed pass reproduces them
+    ref_m = margins[:, :, :n].clone()
     e2e_step()
     torch.cuda.synchronize()
     if dist is not None:
@@ -706,10 +708,15 @@ def run_e2e(args, ko, torch, wl, d, ops, gold, plans, margins, classes, counts, 
     n_all = int(n_all.item())
     h2d = n_pages * page_bytes
     d2h = h_counts.numel() * 8 + h_margins.numel() * 4
+    # grid mode, bitwise: margins are order-independent fixed-order sums, so the streamed pass
+    # must equal the resident one on the same pages (routed calls NaN-fill the margins of tuples
+    # outside their tuple_idx chunk, ko.h, so only the counts are comparable there)
+    same = bool(torch.equal(h_margins[:, :, :n], ref_m.cpu())) if len(plans) != 1 else None
     del host_pool
     return {"value": n_all * args.e2e_steps / (ms / 1000.0), "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
             "ms_per_step": ms / args.e2e_steps, "tuples_per_rank": n,
+            "margins_equal_resident_pass": same,
             "how": "pinned host KV pages -> device in 8 tuple chunks on a copy stream, "
                    "overlapped with ko_score_batch on each landed chunk; counts+margins D2H"}
 
