@@ -141,7 +141,8 @@ typedef struct {
  *     each tuple's cache (nested prefixes: the largest variant's bytes serve all), then every
  *     plan is evaluated per tuple in the same kernel and its counts accumulated.
  *   - n_plans == 1 ("routed mode", P:176-180 cascades): stages execute in order; only tuples
- *     reaching a stage are scored for it (the rest of the margins are left NaN), which is the
+ *     reaching a stage are scored for it (the rest of the processed tuples' KV-variant margins
+ *     are set to NaN; tuples outside tuple_idx and external variants are not touched), which is the
  *     runtime saving cascades exist for.  Each tuple's cache is read once, up to the
  *     largest extent its reached stages need: the plan's operators share one read while they fit
  *     one 16-row tile (an operator's margin may be computed for a tuple that never reaches its

@@ -248,8 +248,10 @@ def score_batch(kv: KVCache, ops: Sequence[Operator], variants: Sequence[Tuple[i
     dev = kv.pool.device
     n_ops, n_var, n = len(ops), len(variants), kv.n_tuples
     routed = plans is not None and len(plans) == 1
-    if margins is None:
-        margins = torch.empty((n_ops, n_var, n), dtype=torch.float32, device=dev)
+    if margins is None:  # with a tuple subset, the tuples outside it read NaN (not scored)
+        margins = (torch.empty if tuple_idx is None else
+                   lambda *a, **k: torch.full(*a, float("nan"), **k))(
+            (n_ops, n_var, n), dtype=torch.float32, device=dev)
     if classes is None and want_classes:
         classes = torch.empty((n_ops, n_var, n), dtype=torch.int32, device=dev)
     n_plans = 0 if plans is None else len(plans)

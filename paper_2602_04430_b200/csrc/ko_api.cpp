@@ -528,12 +528,6 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
 
   // ---- routed mode (cascade execution): only tuples reaching a stage are scored
   const ko_plan& P = plans[0];
-  if (margins)  // unreached entries read NaN; external variants are inputs and stay untouched
-    for (int o = 0; o < n_ops; ++o)
-      for (int v = 0; v < n_variants; ++v)
-        if (!is_external(variants[v]))
-          KO_CUDA(cudaMemsetAsync(margins + ((size_t)o * n_variants + v) * kv->n_tuples, 0xFF,
-                                  sizeof(float) * (size_t)kv->n_tuples, s));
   ko::RouteParams rp;
   std::memset(&rp, 0, sizeof(rp));
   rp.plan = P;

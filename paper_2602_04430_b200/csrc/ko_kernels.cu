@@ -324,6 +324,14 @@ __global__ void __launch_bounds__(kWalkThreads) ko_walk_kernel(const __grid_cons
     int64_t t = 0;
     if (w < n_work) {
       t = p.work ? (int64_t)p.work[w] : w;
+      if (p.pos == 0 && p.margins) {
+        // this call's tuples start with NaN KV-variant margins (only reached entries are
+        // written, §8(b)); tuples outside the call's tuple_idx are not touched
+        for (int o = 0; o < p.n_ops_total; ++o)
+          for (int v = 0; v < p.n_var_total; ++v)
+            if (p.var_rank[v] >= 0)
+              p.margins[((size_t)o * p.n_var_total + v) * p.n_tuples + t] = CUDART_NAN_F;
+      }
       uint32_t state = p.pos == 0 ? 1u : __ldcg(p.tuple_state + t);
       uint32_t done = p.pos == 0 ? 0xFFFFFFFFu : __ldcg(p.tuple_done + t);  // 4-bit round+1 per group
       if (p.group >= 0) {  // −1: a walk-only launch (external stage at position 0) computed nothing

@@ -316,6 +316,16 @@ def test_routed_subset_and_launch_count(ko):
                          cg[:, :, sub], [plan], wl.spec.op_classes, gold[:, sub])
     # C4's plan: one fused group; positions 0, 1, 3, 5 launched (2 and 4 are covered by 0)
     assert launches == 1 + 2 * 4 + 1
+    # caller-owned margins: the tuples outside tuple_idx are not touched (chunked routed calls keep
+    # every chunk's results), the subset's unreached entries read NaN
+    mine = torch.full_like(m, 7.0)
+    ko.score_batch(d["kv"], d["ops"], wl.variants, plans=[plan], gold=d["gold"], margins=mine,
+                   tuple_idx=torch.from_numpy(sub).cuda())
+    torch.cuda.synchronize()
+    mm = mine.cpu().numpy()
+    assert (mm[:, :, outside] == 7.0).all()
+    assert np.array_equal(np.isnan(mm[:, :, sub]), np.isnan(mg[:, :, sub]))
+    assert np.array_equal(mm[:, :, sub][np.isfinite(mm[:, :, sub])], mg[:, :, sub][np.isfinite(mg[:, :, sub])])
 
 
 def test_routed_wide_map_alone(ko):
