@@ -1,4 +1,9 @@
-"""Race / memory / sync checking of every kernel under compute-sanitizer."""
+"""Race / memory / sync checking of every kernel under compute-sanitizer.
+
+Opt-in (KO_RUN_SANITIZER=1): the GPU pool closed compute-sanitizer in round 2 (its wrapper
+refuses with exit code 86, runs under it had left GPUs needing a reset), so the default
+`-m gpu` run skips it.  The clean round-1 runs are in profiles/r01_sanitizer.md; the device-side
+checks of caller data are the KO_DEBUG build (tests/test_debug_build_gpu.py)."""
 import os
 import shutil
 import subprocess
@@ -15,6 +20,8 @@ def test_compute_sanitizer_clean(tool):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
+    if os.environ.get("KO_RUN_SANITIZER") != "1":
+        pytest.skip("compute-sanitizer is closed on this GPU pool; set KO_RUN_SANITIZER=1 to run")
     exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(exe):
         pytest.skip("compute-sanitizer not installed")
@@ -22,5 +29,7 @@ def test_compute_sanitizer_clean(tool):
                         os.path.join(ROOT, "tools", "sanitize_exercise.py")],
                        capture_output=True, text=True, timeout=280)
     out = r.stdout + r.stderr
+    if r.returncode == 86 and "closed" in out:
+        pytest.skip("compute-sanitizer refused by the pool's wrapper: " + out.strip()[-200:])
     assert r.returncode == 0, out[-3000:]
     assert "0 errors" in out or "0 hazards" in out, out[-3000:]
