@@ -99,3 +99,31 @@ def test_build_ties_keep_source_order(ko):
         torch.cuda.synchronize()
         got = dst.view(torch.int16).cpu().numpy().view(np.uint16)
         assert _valid_slots_equal(got, exp, indptr, ids, sl)
+
+
+def test_build_rank_path_every_segment_count(ko):
+    """The short-tuple kernel ranks by merging sorted 64-token segments (1 … 16 segments): every
+    segment count and the lengths around each 64-token boundary and each page boundary, with
+    duplicated rows (equal scores across segments) mixed in, vs the oracle."""
+    rng = np.random.default_rng(23)
+    geom = Geom(1, 2, 1, 128, 1)
+    lengths = [2, 31, 63, 64, 65, 127, 128, 129, 191, 255, 256, 257, 383, 511, 512, 513, 639,
+               767, 768, 895, 1000, 1023, 1024]
+    K, V, _ = random_problem(rng, geom, lengths)
+    for t in range(len(lengths)):                  # ties that straddle segments
+        K[t][..., 7::5, :] = K[t][..., :1, :]
+    pool, indptr, ids, sl = build_pool(K, V, lengths, placement="shuffle", seed=9, poison=True)
+    mu = rng.normal(0, 1, size=(1, 2, 128)).astype(np.float32)
+    s2 = rng.uniform(0, 1, size=(1, 2, 128)).astype(np.float32)
+    dst_ids = np.random.default_rng(3).permutation(len(ids)).astype(np.int32)
+    exp = oracle.build_order(geom, pool, indptr, ids, sl, mu, s2, dst_ids)
+    kv, _ = tensors_to_device(pool, indptr, ids, sl, geom,
+                              [dict(n_classes=1, q=np.zeros((1, 2, 1, 128), np.uint16),
+                                    w=np.zeros((1, 1, 2, 1, 128), np.float32),
+                                    b=np.zeros(1, np.float32))])
+    dst = torch.zeros_like(kv.pool)
+    ko.build_importance_order(kv, torch.from_numpy(mu).cuda(), torch.from_numpy(s2).cuda(), dst,
+                              torch.from_numpy(dst_ids).cuda())
+    torch.cuda.synchronize()
+    got = dst.view(torch.int16).cpu().numpy().view(np.uint16)
+    assert _valid_slots_equal(got, exp, indptr, dst_ids, sl)
