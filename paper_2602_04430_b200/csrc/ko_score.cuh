@@ -369,9 +369,11 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       const bool tail_page = pg * 16 + 16 > n_need;  // warp-uniform
       float Sacc[2][4];
       float U[NT][2][4];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        uint4 kf[KP], vf[KP];
+      // kEarly (one W·V tile, registers to spare): both n-tiles' K/V fragments are read first and
+      // the stage goes back to the TMA before the MMAs; otherwise one n-tile at a time
+      constexpr bool kEarly = NT == 1;
+      uint4 kfa[kEarly ? 2 : 1][KP], vfa[kEarly ? 2 : 1][KP];
+      auto read_frags = [&](int nt, uint4* kf, uint4* vf) {
 #pragma unroll
         for (int j = 0; j < KP; ++j) {
           const uint32_t a = stage + frag_off[j] + nt * 8 * 128;
@@ -384,6 +386,20 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
           for (int j = 0; j < KP; ++j)
             if (!valid) { kf[j] = make_uint4(0, 0, 0, 0); vf[j] = make_uint4(0, 0, 0, 0); }
         }
+      };
+      if constexpr (kEarly) {
+        read_frags(0, kfa[0], vfa[0]);
+        read_frags(1, kfa[1], vfa[1]);
+        __syncwarp();
+        ++consumed;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        refill();
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        uint4* kf = kfa[kEarly ? nt : 0];
+        uint4* vf = vfa[kEarly ? nt : 0];
+        if constexpr (!kEarly) read_frags(nt, kf, vf);
 #pragma unroll
         for (int i = 0; i < 4; ++i) Sacc[nt][i] = 0.f;
 #pragma unroll
@@ -420,10 +436,12 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         }
       }
       // the stage's bytes are in registers: hand the slot back to TMA for page pg + S
-      __syncwarp();
-      ++consumed;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      refill();
+      if constexpr (!kEarly) {
+        __syncwarp();
+        ++consumed;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        refill();
+      }
       // the fragments are dead after the last page's MMAs: fetch the next head's now
       if (pg + 1 == pg1 && hh + 1 < HG) load_frags(h + 1);
       // ---- per-lane token indices and values: k = nt*2 + e ↔ token pg*16 + nt*8 + 2q + e
