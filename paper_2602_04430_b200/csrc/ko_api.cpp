@@ -163,6 +163,11 @@ struct Workspace {
   size_t total;
 };
 
+// Saved softmax state of one lane group for a table of NT W·V tiles: M[2], den[2], acc[2·NT],
+// padded to whole 32-byte sectors (the kernel writes every record as whole sectors: partially
+// written sectors cost the routed C4 round 0 ≈ 1 % — profiles/r02_ab/rstate).
+constexpr int rstate_record_floats(int nt) { return (4 + 2 * nt + 7) / 8 * 8; }
+
 // Layout: [counters 256 B][done][part][qfrag][wfrag][tuple_state][worklist][position
 // worklists][tuple_done][rstate]
 Workspace layout(const ko_kv_cache* kv, int max_cls, int max_ent, int32_t n_ops, int32_t n_variants,
@@ -196,8 +201,8 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int max_ent, int32_t n_ops,
   w.lpt_hist = (int*)take(sizeof(int) * 4097);
   w.lpt_perm = (int32_t*)take(sizeof(int32_t) * (size_t)std::max<int64_t>(n_work, 1));
   // saved softmax states of the routed rounds: a group's table needs ≤ pow2(max entries per row)
-  // tiles, so 4 + 2·that floats per lane group bound every group's state
-  w.rstate_w = 4 + 2 * std::min(ko::kMaxTNT, pow2_at_least(std::max(max_ent, 1)));
+  // tiles, so rstate_record_floats(that) floats per lane group bound every group's record
+  w.rstate_w = rstate_record_floats(std::min(ko::kMaxTNT, pow2_at_least(std::max(max_ent, 1))));
   w.rstate_group = nt * kv->n_layers * kv->n_kv_heads * 8 * (size_t)w.rstate_w;
   w.rstate = (float*)take(sizeof(float) * w.rstate_group * n_ops);
   w.total = off;
@@ -670,7 +675,8 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     for (int q = 0; q < P.n_stages; ++q)
       if (pos_group[q] == g && pos_round[q] > r) sp.save_state = 1;
     sp.rstate = ws.rstate + (size_t)g * ws.rstate_group;
-    sp.rstate_w = ws.rstate_w;
+    sp.rstate_w = rstate_record_floats(NT);  // this group's record (≤ the workspace bound)
+    if (sp.rstate_w > ws.rstate_w) return fail(KO_EWORKSPACE, "routed mode: state record %d > %d", sp.rstate_w, ws.rstate_w);
     sp.pos = pos;
     sp.n_pos = P.n_stages;
     sp.group = walk_only ? -1 : g;  // −1: the walk records no computed round

@@ -111,7 +111,8 @@ struct ScoreParams {
   // margin once var_rank says it is complete).
   int32_t save_state;            // a later rank of this group exists: save the state at the end
   float* rstate;                 // [n_tuples][n_layers][Hkv][8][rstate_w] (this group's slice)
-  int32_t rstate_w;              // floats per lane group: M[2], den[2], acc[2·NT]
+  int32_t rstate_w;              // floats per lane group: M[2], den[2], acc[2·NT], zero-padded
+                                 // to whole 32-byte sectors (= the kernel's kRecW)
   int32_t n_lh_all;              // n_layers · Hkv (partials of walk mode are per tuple, all layers)
   int32_t part_cpr;              // class stride of walk-mode partials (same for every group)
   // table-driven row/class packing (template NT): per lane group g, W·V slot k = 2·tile + hr

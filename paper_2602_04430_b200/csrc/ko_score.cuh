@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   constexpr int KS = D / 16;  // mma k-steps over head_dim
   constexpr int KP = D / 32;  // 128-bit fragment reads per token row per lane (2 k-steps each)
   constexpr int NSL = 2 * NT;                       // table slots per lane
+  constexpr int kRecW = (4 + NSL + 7) / 8 * 8;      // saved-state record (walk), whole sectors
   constexpr int WREG = NT <= 2 ? NT : 0;            // W·V tiles whose fragments stay in registers
   constexpr int S = Ring<D>::kStages;
   constexpr int STAGE = Ring<D>::kStageBytes;
@@ -338,7 +339,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
     int next_snap = first_snap;
     const uint4* wbase = p.wfrag + (size_t)unit_lh * NT * KS * 32 + lane;
     // saved state of (t, l, h) for this lane group (walk mode)
-    float* rst = walk ? p.rstate + ((((size_t)t * p.n_layers + l) * Hkv + h) * 8 + g) * p.rstate_w
+    KO_DCHECK(!walk || p.rstate_w == kRecW);
+    float* rst = walk ? p.rstate + ((((size_t)t * p.n_layers + l) * Hkv + h) * 8 + g) * kRecW
                       : nullptr;
 
     // lane-local online-softmax state per half-slot (log2 domain)
@@ -512,11 +514,25 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
               accm[k] = a;
               val[k] = a * rden[k & 1];
             }
-            if (walk && p.save_state && next_snap == s1 && q == 0) {
-              // end of this round's extent: save the merged state for a later round to resume
-              rst[0] = Mq[0]; rst[1] = Mq[1]; rst[2] = den[0]; rst[3] = den[1];
+            if (walk && p.save_state && next_snap == s1) {
+              // end of this round's extent: save the merged state for a later round to resume.
+              // The quad's 4 lanes hold the same merged values: lane q stores floats 8i + 2q and
+              // 8i + 2q + 1 of the record (zero-padded to kRecW), so each warp store writes whole
+              // 32-byte sectors (partial sectors cost DRAM write amplification)
+              float rec[kRecW];
+              rec[0] = Mq[0]; rec[1] = Mq[1]; rec[2] = den[0]; rec[3] = den[1];
 #pragma unroll
-              for (int k = 0; k < NSL; ++k) rst[4 + k] = accm[k];
+              for (int k = 0; k < NSL; ++k) rec[4 + k] = accm[k];
+#pragma unroll
+              for (int k = 4 + NSL; k < kRecW; ++k) rec[k] = 0.f;
+#pragma unroll
+              for (int i = 0; i < kRecW / 8; ++i) {
+                float a = rec[8 * i], b = rec[8 * i + 1];
+                if (q == 1) { a = rec[8 * i + 2]; b = rec[8 * i + 3]; }
+                if (q == 2) { a = rec[8 * i + 4]; b = rec[8 * i + 5]; }
+                if (q == 3) { a = rec[8 * i + 6]; b = rec[8 * i + 7]; }
+                *reinterpret_cast<float2*>(rst + 8 * i + 2 * q) = make_float2(a, b);
+              }
             }
             // cross-lane-group sum per (op, class) target through shared memory: lane j adds
             // target j's slots in a fixed (ascending) order, then writes its partial
