@@ -189,8 +189,9 @@ Workspace layout(const ko_kv_cache* kv, int max_cls, int max_ent, int32_t n_ops,
   w.round_len = ctr ? (unsigned long long*)(ctr + 64) : nullptr;
   w.done = (int32_t*)take(sizeof(int32_t) * (size_t)std::max<int64_t>(n_work, 1));
   // partials: per work slot (grid) or per tuple (walk: they persist across the rounds of a call)
+  // (walk mode: per tuple and layer·kv-head, n_variants whole-sector blocks of n_ops·CPR floats)
   w.part = (float*)take(sizeof(float) * (size_t)std::max<int64_t>(std::max<int64_t>(n_work, kv->n_tuples), 1) *
-                        kv->n_layers * kv->n_kv_heads * n_ops * n_variants * CPR);
+                        kv->n_layers * kv->n_kv_heads * n_variants * ko::walk_part_blk(n_ops, CPR));
   w.qfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * KS * 32);
   w.wfrag = (uint4*)take(sizeof(uint4) * (size_t)kv->n_layers * kv->n_kv_heads * NT * KS * 32);
   w.tuple_state = (uint32_t*)take(sizeof(uint32_t) * nt);

@@ -115,12 +115,20 @@ struct ScoreParams {
                                  // to whole 32-byte sectors (= the kernel's kRecW)
   int32_t n_lh_all;              // n_layers · Hkv (partials of walk mode are per tuple, all layers)
   int32_t part_cpr;              // class stride of walk-mode partials (same for every group)
+                                 // walk-mode partials: [t][layer·Hkv + h][variant][block], block
+                                 // = [op][part_cpr] padded to whole sectors (walk_part_blk)
   // table-driven row/class packing (template NT): per lane group g, W·V slot k = 2·tile + hr
   // (A-row half hr) accumulates with S row g + 8·hr into the local (op, class) target
   // tgt = op·8 + class (−1: unused)
   int8_t tbl_tgt[8][16];
   ko_plan plans[kMaxPlans];
 };
+
+// Floats per (tuple, layer·kv-head, variant) block of walk-mode partial logits: [op][cpr],
+// padded to whole 32-byte sectors so a snapshot stores its block as whole sectors.
+__host__ __device__ inline int walk_part_blk(int n_ops_total, int cpr) {
+  return (n_ops_total * cpr + 7) / 8 * 8;
+}
 
 struct PrepParams {
   int32_t n_l, n_kv_heads, gqa, n_q, n_layers, head_dim;

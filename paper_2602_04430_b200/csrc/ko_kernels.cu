@@ -277,9 +277,10 @@ __global__ void __launch_bounds__(kReduceThreads, 2) reduce_kernel(const __grid_
 __device__ __forceinline__ float walk_margin(const ScoreParams& p, int64_t t, int o, int v,
                                              int32_t* cls_out) {
   const int CPR = p.part_cpr;  // one class stride for every group's partials
-  const int nzg = p.n_ops_total * p.n_var_total * CPR;
+  const int PB = walk_part_blk(p.n_ops_total, CPR);
+  const int nzg = p.n_var_total * PB;  // floats per (tuple, layer·kv-head)
   const int nu = min(p.cut[p.var_local[v]], p.n_layers) * p.n_kv_heads;  // l-major units
-  const float* src = p.part + (size_t)t * p.n_lh_all * nzg + (size_t)(o * p.n_var_total + v) * CPR;
+  const float* src = p.part + (size_t)t * p.n_lh_all * nzg + (size_t)v * PB + (size_t)o * CPR;
   const int C = p.op_classes_g[o];
   float best = -CUDART_INF_F, second = -CUDART_INF_F;
   int bi = 0;

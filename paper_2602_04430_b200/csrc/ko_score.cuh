@@ -176,6 +176,26 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
         }
   }
 
+  // walk-mode partial blocks ([op][part_cpr], whole sectors): lane j < wblk owns position j =
+  // (caller's op og, class c) — its value is the target sum of lane (local op)·8 + c; zero for
+  // classes past the op's count and for the padding; ops outside this launch: not written
+  const int wblk = walk ? walk_part_blk(p.n_ops_total, p.part_cpr) : 0;
+  int wsrc = 0;
+  bool wown = false, wzero = false;
+  if (lane < wblk) {
+    const int og = lane / p.part_cpr, c = lane - og * p.part_cpr;
+    if (og >= p.n_ops_total) {
+      wown = wzero = true;
+    } else {
+      for (int ol = 0; ol < p.n_ops; ++ol)
+        if (p.op_ids[ol] == og) {
+          wown = true;
+          wzero = c >= p.op_classes[ol];
+          wsrc = wzero ? 0 : ol * 8 + c;
+        }
+    }
+  }
+
   // lane-constant smem offsets of this lane's fragment reads inside a stage: token row g (+8),
   // d-chunk (2q + (j & 1)) of box (j >> 1), XOR-swizzled by the row (= token mod 8)
   uint32_t frag_off[KP];
@@ -552,20 +572,25 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
               for (uint64_t m = red1; m; m &= m - 1) x += sv[64 + __ffsll((long long)m) - 1];
             }
             __syncwarp();
-            if (red_n > 0) {
+            if (walk) {
+              // per tuple (persisting across rounds), caller's (op, variant): lane j stores
+              // position j of the variant's whole-sector block (value of lane wsrc, or zero)
+              const float xv = __shfl_sync(0xffffffffu, x, wsrc);
+              if (wown) {
+#pragma unroll
+                for (int v = 0; v < kMaxVar; ++v)
+                  if (nkv[v] == next_snap)
+                    p.part[(((size_t)t * p.n_lh_all + unit_lh) * p.n_var_total + p.var_ids[v]) * wblk +
+                           lane] = wzero ? 0.f : xv;
+              }
+            } else if (red_n > 0) {
+              // per work slot, local (op, variant): the grid finaliser's layout
               const int o = lane >> 3, c = lane & 7;
 #pragma unroll
               for (int v = 0; v < kMaxVar; ++v)
-                if (nkv[v] == next_snap) {
-                  // walk: per tuple (persisting across rounds), caller's (op, variant); grid: per
-                  // work slot, local (op, variant) — the grid finaliser's layout
-                  const size_t at =
-                      walk ? ((((size_t)t * p.n_lh_all + unit_lh) * p.n_ops_total + p.op_ids[o]) *
-                                  p.n_var_total + p.var_ids[v]) * p.part_cpr + c
-                           : ((((size_t)wslot * p.n_l * Hkv + unit_lh) * p.n_ops + o) * p.n_var + v) *
-                                 CPR + c;
-                  p.part[at] = x;
-                }
+                if (nkv[v] == next_snap)
+                  p.part[((((size_t)wslot * p.n_l * Hkv + unit_lh) * p.n_ops + o) * p.n_var + v) *
+                             CPR + c] = x;
             }
           }
           next_snap = next_point(next_snap);  // the next larger snapshot point
