@@ -523,12 +523,18 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     pp.gplans = ws.gplans;
     pp.n_plans = n_plans;
     for (int g = 0; g < n_plans; ++g) pp.plans[g] = plans[g];
+    static const int fin_env = [] {  // A/B knob: 0 = finalise tuples inside the scoring kernel
+      const char* e = std::getenv("KO_GRID_FIN_KERNEL");
+      return e ? std::atoi(e) : 1;
+    }();
+    sp.fin_kernel = fin_env;
     KO_LAUNCH(ko::launch_prep(pp, s));
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
-    KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
+    if (!sp.fin_kernel) KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));
     if (g_trace_begin) KO_CUDA(cudaEventRecord(g_trace_begin, s));
     KO_LAUNCH(ko::launch_score(sp, kv->head_dim, CPR, NT, n_work * sp.n_l * kv->n_kv_heads, s));
     if (g_trace_end) KO_CUDA(cudaEventRecord(g_trace_end, s));
+    if (sp.fin_kernel) KO_LAUNCH(ko::launch_grid_final(sp, CPR, s));
     return KO_OK;
   }
 

@@ -91,6 +91,7 @@ struct ScoreParams {
   int32_t heads_per_unit;  // kv-heads one work unit streams back-to-back (divides n_kv_heads)
   // grid mode: per-tuple evaluation of every plan (indices are caller's = local here)
   int32_t mode;
+  int32_t fin_kernel;   // grid mode: 1 = tuples finalised by grid_final_kernel after the launch
   int32_t n_plans;
   const uint8_t* gold;  // [n_ops_total][n_tuples] or NULL
   unsigned long long* counts;  // [n_plans][kCountsPerPlan] (int64 bit pattern)
@@ -245,6 +246,8 @@ cudaError_t launch_prep(const PrepParams& p, cudaStream_t s);
 // per-translation-unit instantiations of the scoring kernel (ko_score_d128.cu, ko_score_d64.cu)
 cudaError_t launch_score_d128(const ScoreParams& p, int CPR, int NT, int64_t max_units, cudaStream_t s);
 cudaError_t launch_score_d64(const ScoreParams& p, int CPR, int NT, int64_t max_units, cudaStream_t s);
+// grid-mode tuple finaliser after launch_score (fin_kernel = 1): margins, every plan, counts
+cudaError_t launch_grid_final(const ScoreParams& p, int CPR, cudaStream_t s);
 // scoring kernel with NT table-packed W·V tiles; CPR = class stride of the grid-mode partials
 cudaError_t launch_score(const ScoreParams& p, int head_dim, int CPR, int NT, int64_t max_units,
                          cudaStream_t s);

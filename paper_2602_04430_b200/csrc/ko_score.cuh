@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
   const uint32_t ring_s = smem_u32(ring);
 
   const bool walk = p.mode == MODE_WALK;
-  const int n_cnt_rows = p.mode == MODE_GRID ? p.n_plans : 0;  // walk: ko_walk_kernel counts
+  // walk: ko_walk_kernel counts; grid with fin_kernel: grid_final_kernel counts
+  const int n_cnt_rows = p.mode == MODE_GRID && !p.fin_kernel ? p.n_plans : 0;
   for (int i = threadIdx.x; i < n_cnt_rows * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&s_full[warp][s], 1);
@@ -602,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
    }  // heads of the unit
     // ---- tuple completion (grid mode): the warp finishing the tuple's last unit finalises it;
     // routed rounds are finalised by ko_walk_kernel after the launch
-    if (!walk) {
+    if (!walk && !p.fin_kernel) {
       __syncwarp();
       int last = 0;
       if (lane == 0) {
@@ -661,6 +662,50 @@ cudaError_t launch_score_t(const ScoreParams& p, int64_t max_units, cudaStream_t
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// Grid-mode tuple finaliser as its own launch (fin_kernel = 1): one warp per work slot runs
+// finalise_tuple on the partials the scoring launch left per work slot, so the scoring kernel's
+// warps only stream (the routed mode's ko_walk_kernel split).  Same arithmetic,
+// same fixed summation order: margins and counts are bitwise those of the in-kernel finaliser.
+// ------------------------------------------------------------------------------------------
+constexpr int kFinWarps = 16;
+template <int CPR>
+__global__ void __launch_bounds__(kFinWarps * 32) grid_final_kernel(const __grid_constant__ ScoreParams p) {
+  __shared__ int s_cnt[kMaxPlans * kCountsPerPlan];
+  __shared__ float s_z[kFinWarps][kMaxOps * kMaxVar * kMaxCls];
+  __shared__ float s_m[kFinWarps][kMaxOps * kMaxVar];
+  __shared__ int32_t s_c[kFinWarps][kMaxOps * kMaxVar];
+  for (int i = threadIdx.x; i < p.n_plans * kCountsPerPlan; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n_work = p.work_len_host;
+  for (int64_t w = (int64_t)blockIdx.x * kFinWarps + warp; w < n_work;
+       w += (int64_t)gridDim.x * kFinWarps) {
+    const int64_t t = p.work ? (int64_t)p.work[w] : w;
+    finalise_tuple<CPR>(p, w, t, lane, s_z[warp], s_m[warp], s_c[warp], s_cnt);
+  }
+  flush_counts(s_cnt, p.n_plans, p.counts, p.gold != nullptr);
+}
+
+template <int CPR>
+cudaError_t launch_grid_final_t(const ScoreParams& p, cudaStream_t s) {
+  // latency-bound (L2 loads of the partials, gold, per-tuple plan walks): as many warps as fit
+  static std::atomic<int> occ_of[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 63;
+  int occ = occ_of[dev].load(std::memory_order_relaxed);
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, grid_final_kernel<CPR>, kFinWarps * 32, 0);
+    if (occ < 1) occ = 1;
+    occ_of[dev].store(occ, std::memory_order_relaxed);
+  }
+  const int64_t need = (p.work_len_host + kFinWarps - 1) / kFinWarps;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)num_sms() * occ));
+  grid_final_kernel<CPR><<<(unsigned)grid, kFinWarps * 32, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -16,4 +16,14 @@ cudaError_t launch_score_d128(const ScoreParams& p, int CPR, int NT, int64_t max
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_grid_final(const ScoreParams& p, int CPR, cudaStream_t s) {
+  switch (CPR) {
+    case 1: return launch_grid_final_t<1>(p, s);
+    case 2: return launch_grid_final_t<2>(p, s);
+    case 4: return launch_grid_final_t<4>(p, s);
+    case 8: return launch_grid_final_t<8>(p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace ko
