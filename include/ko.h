@@ -139,7 +139,8 @@ typedef struct {
  *   - n_plans >= 2 or plans on a profiling call ("grid mode", P:281-286 profiling + the 64-point
  *     grid of BASELINE config 5): every (op, variant, tuple) margin is computed in ONE read of
  *     each tuple's cache (nested prefixes: the largest variant's bytes serve all), then every
- *     plan is evaluated per tuple in the same kernel and its counts accumulated.
+ *     plan is evaluated per tuple (by a finaliser launch on the same stream, after the scan) and
+ *     its counts accumulated.
  *   - n_plans == 1 ("routed mode", P:176-180 cascades): stages execute in order; only tuples
  *     reaching a stage are scored for it (the rest of the processed tuples' KV-variant margins
  *     are set to NaN; tuples outside tuple_idx and external variants are not touched), which is the
