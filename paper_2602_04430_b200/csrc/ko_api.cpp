@@ -523,11 +523,15 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
     pp.gplans = ws.gplans;
     pp.n_plans = n_plans;
     for (int g = 0; g < n_plans; ++g) pp.plans[g] = plans[g];
-    static const int fin_env = [] {  // A/B knob: 0 = finalise tuples inside the scoring kernel
+    // Tuple finaliser: its own launch once the scan is long enough for the idle rings it saves
+    // to outweigh one more launch (C5 / C3: −0.4 / −0.6 % per step; C2's 10 k tuples: flat;
+    // C1's 64 tuples: +20 µs), else inside the scoring kernel.  Both are bit-identical
+    // (tests/test_grid_final_gpu.py).  KO_GRID_FIN_KERNEL=0/1 forces one (A/B knob).
+    static const int fin_env = [] {
       const char* e = std::getenv("KO_GRID_FIN_KERNEL");
-      return e ? std::atoi(e) : 1;
+      return e ? std::atoi(e) : -1;
     }();
-    sp.fin_kernel = fin_env;
+    sp.fin_kernel = fin_env >= 0 ? fin_env : (n_work >= 8192 ? 1 : 0);
     KO_LAUNCH(ko::launch_prep(pp, s));
     KO_CUDA(cudaMemsetAsync(ws.unit_counter, 0, 16, s));
     if (!sp.fin_kernel) KO_CUDA(cudaMemsetAsync(ws.done, 0, sizeof(int32_t) * (size_t)n_work, s));

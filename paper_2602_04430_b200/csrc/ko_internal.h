@@ -116,7 +116,7 @@ struct ScoreParams {
                                  // to whole 32-byte sectors (= the kernel's kRecW)
   int32_t n_lh_all;              // n_layers · Hkv (partials of walk mode are per tuple, all layers)
   int32_t part_cpr;              // class stride of walk-mode partials (same for every group)
-                                 // walk-mode partials: [t][layer·Hkv + h][variant][block], block
+                                 // walk-mode partials: [t][variant][layer·Hkv + h][block], block
                                  // = [op][part_cpr] padded to whole sectors (walk_part_blk)
   // table-driven row/class packing (template NT): per lane group g, W·V slot k = 2·tile + hr
   // (A-row half hr) accumulates with S row g + 8·hr into the local (op, class) target

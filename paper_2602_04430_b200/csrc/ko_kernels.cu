@@ -278,9 +278,10 @@ __device__ __forceinline__ float walk_margin(const ScoreParams& p, int64_t t, in
                                              int32_t* cls_out) {
   const int CPR = p.part_cpr;  // one class stride for every group's partials
   const int PB = walk_part_blk(p.n_ops_total, CPR);
-  const int nzg = p.n_var_total * PB;  // floats per (tuple, layer·kv-head)
+  const int nzg = PB;  // floats per (tuple, variant, layer·kv-head) block
   const int nu = min(p.cut[p.var_local[v]], p.n_layers) * p.n_kv_heads;  // l-major units
-  const float* src = p.part + (size_t)t * p.n_lh_all * nzg + (size_t)v * PB + (size_t)o * CPR;
+  const float* src =
+      p.part + ((size_t)t * p.n_var_total + v) * p.n_lh_all * PB + (size_t)o * CPR;
   const int C = p.op_classes_g[o];
   float best = -CUDART_INF_F, second = -CUDART_INF_F;
   int bi = 0;

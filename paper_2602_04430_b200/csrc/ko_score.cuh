@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
 #pragma unroll
                 for (int v = 0; v < kMaxVar; ++v)
                   if (nkv[v] == next_snap)
-                    p.part[(((size_t)t * p.n_lh_all + unit_lh) * p.n_var_total + p.var_ids[v]) * wblk +
+                    p.part[(((size_t)t * p.n_var_total + p.var_ids[v]) * p.n_lh_all + unit_lh) * wblk +
                            lane] = wzero ? 0.f : xv;
               }
             } else if (red_n > 0) {
