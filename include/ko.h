@@ -134,7 +134,7 @@ typedef struct {
  *            n_tuples (n_idx ignored).  n_idx == 0 with a non-NULL tuple_idx is a no-op.
  * margins:   device fp32 [n_ops][n_variants][n_tuples], indexed by tuple id (may be NULL only in
  *            routed mode).  classes: device int32, same shape, argmax class (0 for filters); may
- *            be NULL.
+ *            be NULL; in routed mode only the reached (finite-margin) entries are written.
  * plans[n_plans]: host plan structs; NULL/0 = profiling only.
  *   - n_plans >= 2 or plans on a profiling call ("grid mode", P:281-286 profiling + the 64-point
  *     grid of BASELINE config 5): every (op, variant, tuple) margin is computed in ONE read of
@@ -156,7 +156,8 @@ typedef struct {
  * counts:    device int64 [n_plans][KO_COUNTS_PER_PLAN], accumulated (+=).
  * workspace: device scratch of >= ko_workspace_size(...) bytes, 256-byte aligned (per-tuple
  *            partial logits and, for routed mode, saved softmax states: O(n_tuples · n_layers ·
- *            n_kv_heads · n_ops · (n_variants · classes + 8·(4 + 2·tiles))) floats).
+ *            n_kv_heads · n_ops · (n_variants · classes + 8·(4 + 2·tiles))) floats).  Its
+ *            contents on entry do not matter: a call reads only what it wrote itself.
  * Errors: KO_EINVAL for NULL required pointers, head_dim not in {64,128}, keep_permille outside
  *   [1,1000], layer_cut outside [1,n_layers], theta_lo > theta_hi, a final filter stage with
  *   theta_lo != theta_hi, a referenced op with no final stage or a stage after its final stage,

@@ -39,9 +39,9 @@ def test_routed_c4_with_poisoned_workspace(ko):
         res.append((m.cpu().numpy(), c.cpu().numpy(), counts.cpu().numpy()))
     (m0, c0, k0), (m1, c1, k1) = res
     assert np.array_equal(m0.view(np.uint32), m1.view(np.uint32))
-    assert np.array_equal(c0, c1) and np.array_equal(k0, k1)
+    reached = np.isfinite(m0)                      # classes of unreached entries: unspecified
+    assert np.array_equal(c0[reached], c1[reached]) and np.array_equal(k0, k1)
     m_or, c_or = oracle.score_workload(wl, np.arange(n))
-    reached = np.isfinite(m0)
     # every variant of the plan is reached by some tuple, the large ones only via resumed state
     for o, v, *_ in plan:
         assert reached[o, v].any()
