@@ -393,7 +393,8 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       float Sacc[2][4];
       float U[NT][2][4];
       // kEarly (one W·V tile, registers to spare): both n-tiles' K/V fragments are read first and
-      // the stage goes back to the TMA before the MMAs; otherwise one n-tile at a time
+      // the stage goes back to the TMA before the MMAs; otherwise one n-tile at a time, the
+      // stage handed back once the second n-tile's fragments are read
       constexpr bool kEarly = NT == 1;
       uint4 kfa[kEarly ? 2 : 1][KP], vfa[kEarly ? 2 : 1][KP];
       auto read_frags = [&](int nt, uint4* kf, uint4* vf) {
@@ -422,7 +423,15 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
       for (int nt = 0; nt < 2; ++nt) {
         uint4* kf = kfa[kEarly ? nt : 0];
         uint4* vf = vfa[kEarly ? nt : 0];
-        if constexpr (!kEarly) read_frags(nt, kf, vf);
+        if constexpr (!kEarly) {
+          read_frags(nt, kf, vf);
+          if (nt == 1) {  // the stage's last reads are issued: hand it back before these MMAs
+            __syncwarp();
+            ++consumed;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            refill();
+          }
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) Sacc[nt][i] = 0.f;
 #pragma unroll
@@ -457,13 +466,6 @@ __global__ void __launch_bounds__(kThreads, 2) ko_score_kernel(const __grid_cons
             mma16816(U[tt][nt], a1[0], a1[1], a1[2], a1[3], vf[j].z, vf[j].w);
           }
         }
-      }
-      // the stage's bytes are in registers: hand the slot back to TMA for page pg + S
-      if constexpr (!kEarly) {
-        __syncwarp();
-        ++consumed;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        refill();
       }
       // the fragments are dead after the last page's MMAs: fetch the next head's now
       if (pg + 1 == pg1 && hh + 1 < HG) load_frags(h + 1);
