@@ -654,11 +654,32 @@ ko_status ko_score_batch(const ko_kv_cache* kv, const ko_operator* ops, int32_t 
   // nothing: position 0 on one only walks every tuple (deciding it from the caller's margins and
   // queueing the survivors), and a later one never receives a tuple (its margin is always
   // available).  A KV position whose (group, round) position 0 already streamed is covered.
-  auto launched = [&](int pos) {
-    if (pos == 0) return true;
-    if (pos_round[pos] < 0) return false;
-    return !(pos_round[0] >= 0 && pos_group[pos] == pos_group[0] && pos_round[pos] <= pos_round[0]);
+  auto covered = [&](int pos) {
+    if (pos == 0) return false;
+    if (pos_round[pos] < 0) return true;
+    return pos_round[0] >= 0 && pos_group[pos] == pos_group[0] && pos_round[pos] <= pos_round[0];
   };
+  // Which positions can receive tuples at all: a walk after position w queues a tuple only to
+  // the FIRST later position computing the (group, rank) of the stage it stopped at, and only
+  // for a (group, rank) not yet computed for it — w's own group up to w's rank and position 0's
+  // group up to its rank are (position 0 processes every tuple).  A superset of the real
+  // traffic, so skipping the rest never drops a tuple (C4: positions 3 and 5 repeat position
+  // 1's (group, rank 1) and would only ever run empty).
+  bool receives[KO_MAX_STAGES] = {false};
+  receives[0] = true;
+  for (int w = 0; w < P.n_stages; ++w) {
+    if (!receives[w] || covered(w)) continue;
+    for (int s2 = 0; s2 < P.n_stages; ++s2) {
+      const int g2 = pos_group[s2], rk = pos_round[s2];
+      if (rk < 0) continue;                                        // external: always there
+      if (pos_round[w] >= 0 && g2 == pos_group[w] && rk <= pos_round[w]) continue;
+      if (pos_round[0] >= 0 && g2 == pos_group[0] && rk <= pos_round[0]) continue;
+      int q = w + 1;
+      while (q < P.n_stages && !(pos_group[q] == g2 && pos_round[q] >= rk)) ++q;
+      if (q < P.n_stages) receives[q] = true;
+    }
+  }
+  auto launched = [&](int pos) { return !covered(pos) && receives[pos]; };
   int last_launch = 0, prepped_group = -1;
   for (int pos = 0; pos < P.n_stages; ++pos)
     if (launched(pos)) last_launch = pos;

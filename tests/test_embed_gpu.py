@@ -84,9 +84,10 @@ def test_embedding_first_stage_cascade(ko):
                                   gold=d["gold"])
     torch.cuda.synchronize()
     # the embedding stage at position 0 streams no KV: a walk-only launch decides every tuple from
-    # the caller's margins and queues the survivors; then F1's and F2's gold positions (prep once,
-    # score + walk each) and the final counts
-    assert ko.last_launch_count() == 1 + 3 + 2 + 1
+    # the caller's margins and queues the survivors; then F1's gold position (prep, score, walk —
+    # its fused read also completes F2's gold margin, so F2's position never receives a tuple and
+    # is not launched) and the final counts
+    assert ko.last_launch_count() == 1 + 3 + 1
     mg, cg = m.cpu().numpy(), c.cpu().numpy()
     m_or, c_or = oracle.score_workload(wl, np.arange(n))
     m_all = np.concatenate([m_or, emb[:, None, :]], axis=1)

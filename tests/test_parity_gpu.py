@@ -314,8 +314,9 @@ def test_routed_subset_and_launch_count(ko):
     parity.assert_margins(mg[:, :, sub], m_or[:, :, sub], mask=np.isfinite(mg[:, :, sub]))
     parity.assert_counts(counts.cpu().numpy(), m_or[:, :, sub], c_or[:, :, sub], mg[:, :, sub],
                          cg[:, :, sub], [plan], wl.spec.op_classes, gold[:, sub])
-    # C4's plan: one fused group; positions 0, 1, 3, 5 launched (2 and 4 are covered by 0)
-    assert launches == 1 + 2 * 4 + 1
+    # C4's plan: one fused group; positions 0 and 1 launched (2 and 4 are covered by 0; 3 and 5
+    # would only repeat position 1's (group, rank 1), so no walk can queue a tuple to them)
+    assert launches == 1 + 2 * 2 + 1
     # caller-owned margins: the tuples outside tuple_idx are not touched (chunked routed calls keep
     # every chunk's results), the subset's unreached entries read NaN
     mine = torch.full_like(m, 7.0)
