@@ -124,12 +124,33 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_kernel(const __grid_co
 #else
 #define PROF_MARK(i) do {} while (0)
 #endif
-  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+  __shared__ int s_first;
+  for (int64_t u0 = blockIdx.x;;) {
+    // this CTA's next unit (stride gridDim.x) whose tuple this launch builds — MINT < L ≤ MAXT;
+    // the other launch's (or > 4096: documented, skipped) are passed over 256 candidates per
+    // round, one seq_len load per thread, instead of one dependent load per unit
+    int64_t u = -1;
+    for (int64_t base = u0; base < n_units && u < 0;
+         base += (int64_t)kBuildThreads * gridDim.x) {
+      const int64_t c = base + (int64_t)threadIdx.x * gridDim.x;
+      bool ok = false;
+      if (c < n_units) {
+        const int Lc = p.seq_len[c / (Lyr * H)];
+        KO_DCHECK(Lc >= 1);
+        ok = Lc > MINT && Lc <= MAXT;
+      }
+      __syncthreads();  // the previous round's s_first is read (and the previous unit is done)
+      if (threadIdx.x == 0) s_first = 0x7fffffff;
+      __syncthreads();
+      if (ok) atomicMin(&s_first, (int)threadIdx.x);
+      __syncthreads();
+      if (s_first != 0x7fffffff) u = base + (int64_t)s_first * gridDim.x;
+    }
+    if (u < 0) break;
+    u0 = u + gridDim.x;
     const int64_t t = u / (Lyr * H);
     const int l = (int)((u / H) % Lyr), h = (int)(u % H);
     const int L = p.seq_len[t];
-    KO_DCHECK(L >= 1);
-    if (L <= MINT || L > MAXT) continue;  // the other launch's (or > 4096: documented, skipped)
     const int n_pg = (L + 15) >> 4;
     __syncthreads();  // the previous unit's keys / page ids are dead
     const int64_t pbase = p.indptr[t];
